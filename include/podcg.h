@@ -1,0 +1,198 @@
+/*
+ * podcg.h -- C-ABI of the B200-native POD-augmented CG hot path.
+ *
+ * The reference (recykl, pure Python on numpy/scipy) has no FFI of its own;
+ * every entry point below replaces one numpy/scipy call site on the hot path
+ * and is cited against that site (paths under the reference's pkg/src/recykl).
+ * INTEGRATION.md shows the ctypes stubs a maintainer of the reference would
+ * add to bind these.
+ *
+ * Conventions:
+ *   - every pointer is DEVICE memory owned by the caller (torch tensors);
+ *   - dense N x m blocks are column-major with leading dimension ld >= N;
+ *     the DMMA kernels additionally want ld even and 16-byte aligned columns
+ *     (the host layer pads to multiples of 32 rows);
+ *   - scalars that feed later kernels stay in device memory; nothing here
+ *     synchronises the stream;
+ *   - no allocation visible to the caller: reductions use the caller's
+ *     workspace (double partials + uint32 tickets that start at zero and are
+ *     left at zero);
+ *   - all reductions are deterministic (fixed-order partial combine, no fp64
+ *     atomics), so two runs on the same inputs are bitwise identical;
+ *   - the last argument of every launcher is the cudaStream_t (as void*);
+ *   - return 0 on success, < 0 on error; rk_last_error() gives a
+ *     thread-local message.  Every entry point is re-entrant.
+ */
+#ifndef PODCG_H
+#define PODCG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  RK_OK = 0,
+  RK_ERR_DIMENSION = -1, /* maps to recykl.errors.DimensionMismatch */
+  RK_ERR_NOT_SPD = -2,   /* maps to recykl.errors.NotPositiveDefinite */
+  RK_ERR_CUDA = -3,      /* CUDA launch/runtime error */
+  RK_ERR_ARG = -4        /* bad argument (null pointer, misalignment) */
+};
+
+/* Immutable CSR descriptor borrowing caller-owned device arrays.
+ * Replaces SparseSpdMatrix's scipy csr_matrix (linalg.py:63-135); indices
+ * are int32 (nnz < 2^31 for every configuration). */
+typedef struct rk_csr {
+  int64_t n;
+  int64_t nnz;
+  const int32_t* rowptr; /* n+1 */
+  const int32_t* col;    /* nnz, sorted within each row */
+  const double* val;     /* nnz */
+  int32_t lanes;         /* lanes cooperating on one row: 1,2,4,8,16,32 (0 = auto) */
+  int32_t pad_;
+} rk_csr;
+
+/* Device-resident state of one augmented-PCG run (krylov.py:267-345). */
+typedef struct rk_pcg_state {
+  int64_t k;          /* completed iterations; p_k = V[:, k] is the live direction */
+  int64_t done;       /* 1 once converged or broken down: later kernels are no-ops */
+  int64_t status;     /* 0 running, 1 converged, 2 breakdown (krylov.py:303-304) */
+  int64_t bd_iter;    /* iteration of the breakdown */
+  double rz;          /* r'z of the live direction */
+  double gamma;       /* p'Ap of the live direction */
+  double pp;          /* p'p (breakdown scale) */
+  double alpha;       /* rz / gamma */
+  double rr;          /* ||r||^2 after the last update */
+  double beta;        /* rz_next / rz (cg mode) */
+  double threshold;   /* exit threshold on ||r|| (krylov.py:267) */
+  double rz_next;     /* r'z of the new residual */
+} rk_pcg_state;
+
+/* Everything one augmented-PCG iteration touches.  Replaces the loop body of
+ * augmented_pcg (krylov.py:300-340) with device kernels:
+ *   K1  Ap = A p_k, gamma = p'Ap, p'p, breakdown test, alpha  (krylov.py:301-305)
+ *   K3  x += alpha p; r -= alpha Ap; z = M^{-1} r; ||r||, r'z  (krylov.py:306-321)
+ *   K4  c = cross' z and mu = F^{-1} c                         (krylov.py:155-156,322)
+ *   K5  p_{k+1} = z + beta p_k - B mu  (cg)                     (krylov.py:323-326)
+ *       p_{k+1} = z - B mu, then 2 block-CGS sweeps (fom)       (krylov.py:327-337)
+ *       p_{k+1} = z - B mu + sum_i rz'/rz_i p_i  (fom, paper beta) (krylov.py:329-331) */
+typedef struct rk_pcg_plan {
+  int64_t n;
+  rk_csr A;                 /* A.rowptr == NULL: generic operator, caller fills AV */
+  double* x;
+  double* r;
+  double* z;
+  double* V;                /* directions, column k = p_k */
+  int64_t ldv;
+  int64_t vcap;             /* allocated columns of V (and AV when ldav > 0) */
+  double* AV;               /* A p_k: column k (ldav > 0, kept) or one vector (ldav == 0) */
+  int64_t ldav;
+  const double* dinv;       /* Jacobi inverse diagonal; NULL = no preconditioner */
+  int64_t m;                /* projection width (0 = no augmenting basis) */
+  const double* B;          /* augmenting basis, N x m */
+  int64_t ldb;
+  const double* cross;      /* cached A*B, N x m (DirectReducedProjection.cross) */
+  int64_t ldc;
+  const double* L;          /* dense lower Cholesky factor of the leading wchol block */
+  int64_t ldl;
+  int64_t wchol;
+  const double* sqd;        /* sqrt-diagonal factor blocks for rows wchol..m-1 */
+  double* mu;               /* m */
+  double* coef;             /* vcap: block-CGS coefficients */
+  rk_pcg_state* st;
+  double* alpha_h;          /* vcap */
+  double* gamma_h;          /* vcap */
+  double* rz_h;             /* vcap */
+  double* res_h;            /* vcap + 1: residual norms, res_h[0] = ||r_0|| */
+  double* partials;         /* workspace, rk_pcg_workspace_doubles() */
+  int64_t partials_len;
+  uint32_t* tickets;        /* 8 zero-initialised counters */
+  int32_t mode;             /* 0 cg, 1 fom (two CGS sweeps), 2 fom with paper beta */
+  int32_t pad_;
+} rk_pcg_plan;
+
+const char* rk_last_error(void);
+int rk_device_sm_count(void);
+
+/* Doubles of workspace a plan needs for n rows, projection width m, vcap columns. */
+int64_t rk_pcg_workspace_doubles(int64_t n, int64_t m, int64_t vcap);
+/* Doubles of workspace the reductions below need for n rows / m columns. */
+int64_t rk_reduce_workspace_doubles(int64_t n, int64_t m);
+/* Doubles of split-K workspace rk_gram needs. */
+int64_t rk_gram_workspace_doubles(int64_t n, int64_t m1, int64_t m2);
+
+/* ---- augmented PCG (krylov.py:181-345) ------------------------------------ */
+/* Entry: z = M^{-1} r0, rz, ||r0|| into res_h[0], mu = F^{-1} cross'z, p_0 = z - B mu
+ * (krylov.py:268,290-292). Sets st->rz and st->rr; leaves st->k = 0. */
+int rk_pcg_entry(const rk_pcg_plan* plan, void* stream);
+/* nsteps full iterations for a CSR operator (K1,K3,K4,K5 per step); steps after
+ * convergence/breakdown are no-ops, so the host may overshoot. */
+int rk_pcg_steps(const rk_pcg_plan* plan, int32_t nsteps, int64_t kmax_hint, void* stream);
+/* Generic-operator pieces (ReducedSpdOperator, krylov.py:60-83): the caller writes
+ * A p_k into AV column k (or the AV vector), then calls these three in order. */
+int rk_pcg_curvature(const rk_pcg_plan* plan, void* stream);
+int rk_pcg_update(const rk_pcg_plan* plan, void* stream);
+int rk_pcg_direction(const rk_pcg_plan* plan, int64_t kmax_hint, void* stream);
+
+/* ---- sparse kernels (linalg.py:138-174, preconditioners.py:50-61) -------- */
+/* y = A x (linalg.py:138-148, scipy csr_matvec). */
+int rk_spmv(const rk_csr* A, const double* x, double* y, void* stream);
+/* Y = A X for m columns (linalg.py:173, scipy csr_matvecs). */
+int rk_spmm(const rk_csr* A, int64_t m, const double* X, int64_t ldx, double* Y,
+            int64_t ldy, void* stream);
+/* diag(A) and 1/diag(A); *bad_row (device int64) = first row with diag <= 0, or -1
+ * (preconditioners.py:54-58, linalg.py:114-119). */
+int rk_csr_diagonal(const rk_csr* A, double* diag, double* dinv, int64_t* bad_row,
+                    void* stream);
+/* Largest |A_ij - A_ji| over stored entries and max|A_ij| (device doubles [2]);
+ * replaces the scipy transpose difference of SparseSpdMatrix._validate
+ * (linalg.py:105-113). Requires sorted columns. */
+int rk_csr_asymmetry(const rk_csr* A, double* out2, double* ws, int64_t ws_len,
+                     uint32_t* tickets, void* stream);
+
+/* ---- dense tall-skinny kernels (krylov.py:80-81,151-156,291,326; linalg.py:174;
+ *      pod.py:91-93) ---------------------------------------------------------- */
+/* out[0:m] = B' x (deterministic split reduction). */
+int rk_gemv_t(int64_t n, int64_t m, const double* B, int64_t ldb, const double* x,
+              double* out, double* ws, int64_t ws_len, void* stream);
+/* y = B c (op 0), y = y0 + B c (op 1), y = y0 - B c (op 2); y may alias y0. */
+int rk_gemv_n(int64_t n, int64_t m, const double* B, int64_t ldb, const double* c,
+              const double* y0, double* y, int32_t op, void* stream);
+/* out[0] = x'y (deterministic). */
+int rk_dot(int64_t n, const double* x, const double* y, double* out, double* ws,
+           int64_t ws_len, uint32_t* tickets, void* stream);
+/* Out[:, j] = V[:, j] / s[j] (threestage.py:482-483). */
+int rk_scale_columns(int64_t n, int64_t m, const double* V, int64_t ldv, const double* s,
+                     double* out, int64_t ldo, void* stream);
+/* y = a x + b y with numpy's rounding (no fma contraction). */
+int rk_axpby(int64_t n, double a, const double* x, double b, double* y, void* stream);
+/* y = x0 - y (b - A x, krylov.py:263, threestage.py:277) */
+int rk_sub_from(int64_t n, const double* x0, double* y, void* stream);
+
+/* ---- FP64 tensor-core (DMMA) contractions ---------------------------------- */
+/* G (m1 x m2, col-major ldg) = X' Y, X: N x m1, Y: N x m2 (linalg.py:174
+ * `B.T @ AB`, krylov.py:152, threestage.py:320). Split-K over N with a fixed-order
+ * combine. ws: rk_gram_workspace_doubles(n, m1, m2). */
+int rk_gram(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m2,
+            const double* Y, int64_t ldy, double* G, int64_t ldg, double* ws,
+            int64_t ws_len, void* stream);
+/* Out (N x y) = S (N x s) C (s x y) (pod.py:91-93 `S @ coef`). */
+int rk_gemm_nn(int64_t n, int64_t s, int64_t y, const double* S, int64_t lds,
+               const double* C, int64_t ldc, double* Out, int64_t ldo, void* stream);
+
+/* ---- measurement hooks (bench.py only; not thread-safe) --------------------
+ * Between begin and end, rk_pcg_steps brackets each of its three kernels
+ * (0: K1 SpMV+curvature, 1: K3/K4 update+projection, 2: K5 direction) with
+ * CUDA events on the launching stream; end synchronises and returns the
+ * summed milliseconds and launch counts per kernel. */
+int rk_profile_begin(void);
+/* Number of kernels this library has launched since it was loaded. */
+int64_t rk_launch_count(void);
+int rk_profile_end(double* ms3, int64_t* count3);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PODCG_H */

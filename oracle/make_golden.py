@@ -1,0 +1,244 @@
+"""Generate golden vectors by running the REFERENCE itself (test infrastructure).
+
+Imports ``recykl`` from /root/reference/pkg/src (read-only, in this container
+only), runs its public API on seeded inputs and writes small compressed
+fixtures to tests/golden/. The GPU box never reads /root/reference: the tests
+there only read these committed fixtures.
+
+    python oracle/make_golden.py            # rewrites tests/golden/*.npz
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+REF_SRC = "/root/reference/pkg/src"
+REF_FIX = "/root/reference/pkg/tests/fixtures"
+HERE = os.path.dirname(os.path.abspath(__file__))
+OUT = os.path.join(os.path.dirname(HERE), "tests", "golden")
+sys.path.insert(0, os.path.dirname(HERE))
+
+
+def _ref():
+    if REF_SRC not in sys.path:
+        sys.path.insert(0, REF_SRC)
+    import recykl  # noqa: F401
+
+    return recykl
+
+
+def _pack_sequence(seq, prefix):
+    d = {}
+    for j, spec in enumerate(seq, start=1):
+        A = spec.A
+        d[f"{prefix}A{j}_rowptr"] = np.asarray(A.row_offsets, dtype=np.int64)
+        d[f"{prefix}A{j}_col"] = np.asarray(A.col_indices, dtype=np.int64)
+        d[f"{prefix}A{j}_val"] = np.asarray(A.values, dtype=np.float64)
+        d[f"{prefix}b{j}"] = np.asarray(spec.b, dtype=np.float64)
+        d[f"{prefix}tol{j}"] = np.float64(spec.tol)
+    d[f"{prefix}p"] = np.int64(len(list(seq)))
+    d[f"{prefix}n"] = np.int64(seq.n)
+    return d
+
+
+def _pack_run(solutions, reports, prefix):
+    d = {}
+    for key in ("stage3_iters", "stage2_iters", "stage1_dim", "matvecs", "precond_applies", "final_residual",
+                "truncated", "converged"):
+        d[f"{prefix}{key}"] = np.asarray([getattr(r, key) for r in reports])
+    for j, x in enumerate(solutions, start=1):
+        d[f"{prefix}x{j}"] = np.asarray(x, dtype=np.float64)
+    return d
+
+
+def run_fixture_cases(rk):
+    """Replay the reference's frozen fixture cases with the reference and keep
+    the inputs (its xorshift generator is not part of the product)."""
+    from recykl import preconditioners
+    from recykl.problems import gen_diffusion_sequence
+    from recykl.threestage import SolverConfig, run_sequence
+    from recykl.truncation import TruncationConfig
+
+    out = {}
+    for name in ("identity_like", "invariant_matrix", "drifting_pod"):
+        with open(os.path.join(REF_FIX, f"{name}.json")) as fh:
+            payload = json.load(fh)
+        case = payload["case"]
+        gen = dict(case["generator"])
+        gen["grid"] = tuple(gen["grid"])
+        seq = gen_diffusion_sequence(**gen)
+        variants = {"": dict(mode="fom")}
+        if name == "drifting_pod":
+            variants.update({
+                "cg_": dict(mode="cg"),
+                "paper_": dict(mode="fom", paper=True),
+            })
+        d = _pack_sequence(seq, "")
+        d["frozen_json"] = np.asarray(json.dumps(payload))
+        for tag, v in variants.items():
+            cfg = SolverConfig(truncation=TruncationConfig(**case["config"]), mode=v["mode"])
+            pf = None
+            if case["precond"] != "identity":
+                pf = lambda A, kind=case["precond"]: preconditioners.build(kind, A)
+            else:
+                pf = lambda A: preconditioners.build("identity", A)
+            if v.get("paper"):
+                continue  # paper_fom_beta is not reachable through run_sequence
+            xs, reps, _ = run_sequence(seq, cfg, precond_factory=pf)
+            d.update(_pack_run(xs, reps, tag))
+        out[name] = d
+    return out
+
+
+def run_stage_variants(rk):
+    """drifting-like sequences that exercise stage 2 (stage1_dim < y) and phi = 1."""
+    from recykl import preconditioners
+    from recykl.problems import gen_diffusion_sequence
+    from recykl.threestage import SolverConfig, run_sequence
+    from recykl.truncation import TruncationConfig
+
+    seq = gen_diffusion_sequence((10, 10), p=5, delta=0.05, seed=37, tol=1e-9)
+    d = _pack_sequence(seq, "")
+    pf = lambda A: preconditioners.build("jacobi", A)  # noqa: E731
+    cases = {
+        "s2_": dict(tr=dict(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, stage1_dim=4, storage_cap=30, max_dim=20),
+                    mode="fom"),
+        "s2cg_": dict(tr=dict(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, stage1_dim=4, storage_cap=30, max_dim=20),
+                      mode="cg"),
+        "phi1_": dict(tr=dict(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, stage1_dim=4, full_orth=True,
+                              storage_cap=30, max_dim=20), mode="fom"),
+        "prev_": dict(tr=dict(strategy="pod-a-prev", nu_y=0.999, nu_w=0.9, storage_cap=25, max_dim=12),
+                      mode="cg"),
+        "none_": dict(tr=dict(strategy="none", nu_w=1.0), mode="fom"),
+    }
+    for tag, c in cases.items():
+        cfg = SolverConfig(truncation=TruncationConfig(**c["tr"]), mode=c["mode"])
+        xs, reps, _ = run_sequence(seq, cfg, precond_factory=pf)
+        d.update(_pack_run(xs, reps, tag))
+    return {"stage_variants": d}
+
+
+def run_c1(rk, p=20):
+    """C1 recipe through the reference, both modes."""
+    from recykl import preconditioners
+    from recykl.linalg import SparseSpdMatrix
+    from recykl.problems import LinearSystemSpec, SystemSequence
+    from recykl.threestage import SolverConfig, run_sequence
+    from recykl.truncation import TruncationConfig
+
+    from paper_1512_05820_b200.problems import poisson2d_sequence
+
+    mine = poisson2d_sequence(64, p=p)
+    A0 = mine[0].A
+    A = SparseSpdMatrix(A0.n, A0.row_offsets, A0.col_indices, A0.values)
+    seq = SystemSequence(n=mine.n, systems=[LinearSystemSpec(A=A, b=s.b, xbar=None, tol=s.tol) for s in mine])
+    pf = lambda M: preconditioners.build("jacobi", M)  # noqa: E731
+    d = {"c": mine.C[0], "p": np.int64(p)}
+    for tag, mode, extra in (("fom_", "fom", {}), ("cg_", "cg", {}), ("s5_", "fom", {"stage1_dim": 5})):
+        tr = dict(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=20, max_dim=20, **extra)
+        cfg = SolverConfig(truncation=TruncationConfig(**tr), mode=mode)
+        xs, reps, _ = run_sequence(seq, cfg, precond_factory=pf)
+        r = _pack_run(xs, reps, tag)
+        for j in range(1, len(xs) + 1):
+            r[f"{tag}q{j}"] = np.float64(mine.C[0] @ xs[j - 1])
+            if j > 3:
+                del r[f"{tag}x{j}"]   # keep the fixture small: x for the first 3 systems, q for all
+        d.update(r)
+    return {"c1": d}
+
+
+def run_elasticity(rk):
+    """A 4x4x4-element C3-like elasticity sequence through the reference."""
+    from recykl import preconditioners
+    from recykl.linalg import SparseSpdMatrix
+    from recykl.problems import LinearSystemSpec, SystemSequence
+    from recykl.threestage import SolverConfig, run_sequence
+    from recykl.truncation import TruncationConfig
+
+    from paper_1512_05820_b200.problems import elasticity_sequence
+
+    mine = elasticity_sequence((4, 4, 4), p=4, rtol=1e-8, seed=11)
+    specs = list(mine)
+    seq = SystemSequence(n=mine.n, systems=[
+        LinearSystemSpec(A=SparseSpdMatrix(s.A.n, s.A.row_offsets, s.A.col_indices, s.A.values), b=s.b,
+                         xbar=None, tol=s.tol) for s in specs])
+    pf = lambda M: preconditioners.build("jacobi", M)  # noqa: E731
+    d = {"n": np.int64(mine.n), "c": mine.C[0]}
+    for j, s in enumerate(specs, start=1):
+        d[f"val{j}"] = s.A.values
+        d[f"b{j}"] = s.b
+        d[f"tol{j}"] = np.float64(s.tol)
+    d["rowptr"] = specs[0].A.row_offsets
+    d["col"] = specs[0].A.col_indices
+    for tag, mode in (("cg_", "cg"), ("fom_", "fom")):
+        cfg = SolverConfig(truncation=TruncationConfig(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=12,
+                                                       max_dim=12), mode=mode)
+        xs, reps, _ = run_sequence(seq, cfg, precond_factory=pf)
+        d.update(_pack_run(xs, reps, tag))
+    return {"elasticity": d}
+
+
+def run_kernels(rk):
+    """Kernel-level goldens: spmv, assemble_gram, pod_evd_from_gram, augmented_pcg."""
+    from recykl.krylov import augmented_pcg
+    from recykl.linalg import SparseSpdMatrix, assemble_gram, spmv
+    from recykl.pod import pod_evd_from_gram
+
+    rng = np.random.default_rng(123)
+    n = 300
+    M = np.where(rng.random((n, n)) < 0.04, rng.standard_normal((n, n)), 0.0)
+    M = 0.5 * (M + M.T)
+    np.fill_diagonal(M, np.abs(M).sum(axis=1) + 1.0)
+    A = SparseSpdMatrix.from_dense(M)
+    x = rng.standard_normal(n)
+    S = rng.standard_normal((n, 24))
+    G, AS = assemble_gram(A, S)
+    gamma = 0.5 + rng.random(24)
+    pod = pod_evd_from_gram(G, S, gamma, 0.999)
+    b = rng.standard_normal(n)
+    Y = rng.standard_normal((n, 5))
+    Ad = A.to_dense()
+    yhat0 = np.linalg.solve(Y.T @ Ad @ Y, Y.T @ b)
+    out = {"rowptr": A.row_offsets, "col": A.col_indices, "val": A.values, "x": x, "Ax": spmv(A, x), "S": S,
+           "G": G, "AS": AS, "gamma": gamma, "pod_sigma": pod.singular_values, "pod_y": np.int64(pod.y),
+           "pod_basis": pod.columns, "b": b, "Y": Y, "yhat0": yhat0}
+    for mode in ("cg", "fom"):
+        res = augmented_pcg(A, b, yhat0, Y, tol=1e-10, mode=mode, max_iter=400)
+        out[f"{mode}_k"] = np.int64(res.k)
+        out[f"{mode}_x"] = res.x
+        out[f"{mode}_vhat"] = res.vhat
+        out[f"{mode}_gamma"] = res.gamma
+        out[f"{mode}_hist"] = res.residual_history
+    from recykl.errors import NotConverged
+
+    try:
+        res = augmented_pcg(A, b, yhat0, Y, tol=1e-6, mode="fom", paper_fom_beta=True, max_iter=25)
+        conv = True
+    except NotConverged as exc:
+        res, conv = exc.partial, False
+    out["paper_k"], out["paper_x"], out["paper_conv"] = np.int64(res.k), res.x, np.bool_(conv)
+    out["paper_hist"] = res.residual_history
+    return {"kernels": out}
+
+
+def main():
+    rk = _ref()
+    os.makedirs(OUT, exist_ok=True)
+    blobs = {}
+    blobs.update(run_fixture_cases(rk))
+    blobs.update(run_stage_variants(rk))
+    blobs.update(run_kernels(rk))
+    blobs.update(run_elasticity(rk))
+    blobs.update(run_c1(rk))
+    for name, d in blobs.items():
+        path = os.path.join(OUT, f"{name}.npz")
+        np.savez_compressed(path, **d)
+        print(f"wrote {path} ({os.path.getsize(path) / 1024:.0f} KiB)")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,106 @@
+// Shared device helpers: deterministic warp/block/grid reductions, error plumbing.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/podcg.h"
+
+namespace rk {
+
+constexpr int kWarp = 32;
+constexpr unsigned kFull = 0xffffffffu;
+
+// Xor butterfly: every lane ends with the bitwise-identical sum.
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// Block-wide sum of NV values; result valid in every thread. scratch >= 32*NV.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) v[j] = warp_sum(v[j]);
+  __syncthreads();  // scratch may still be read by a previous call
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) scratch[j * 32 + warp] = v[j];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    double t = (lane < nw) ? scratch[j * 32 + lane] : 0.0;
+    v[j] = warp_sum(t);
+  }
+}
+
+// Publish this block's partials and find out whether it is the last block to
+// finish. partials is [gridDim.x][nv]; the ticket is reset by the last block.
+__device__ __forceinline__ bool publish_and_check_last(const double* vals, int nv,
+                                                       double* partials, uint32_t* ticket) {
+  __shared__ bool s_last;
+  for (int j = threadIdx.x; j < nv; j += blockDim.x)
+    partials[(int64_t)blockIdx.x * nv + j] = vals[j];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = atomicAdd(ticket, 1u);
+    s_last = (t == gridDim.x - 1);
+    if (s_last) *ticket = 0u;
+  }
+  __syncthreads();
+  if (s_last) __threadfence();
+  return s_last;
+}
+
+// Last block: out[j] = sum over blocks (fixed order) of partials[b][j], j < nv.
+// One warp per value, lanes stride over blocks, then a butterfly: deterministic.
+__device__ __forceinline__ void combine_partials(const double* partials, int nb, int nv,
+                                                 double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  for (int j = warp; j < nv; j += nw) {
+    double acc = 0.0;
+    for (int b = lane; b < nb; b += 32) acc += __ldcg(partials + (int64_t)b * nv + j);
+    acc = warp_sum(acc);
+    if (lane == 0) out[j] = acc;
+  }
+  __syncthreads();
+}
+
+// Marks a ticket-synchronised completion without data (used to advance state).
+__device__ __forceinline__ bool ticket_last(uint32_t* ticket) {
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    uint32_t t = atomicAdd(ticket, 1u);
+    s_last = (t == gridDim.x - 1);
+    if (s_last) *ticket = 0u;
+  }
+  __syncthreads();
+  return s_last;
+}
+
+}  // namespace rk
+
+// Host-side helpers shared by the launchers.
+namespace rkh {
+void set_error(const char* fmt, ...);
+void note_launch();  // process-wide count of kernels launched (rk_launch_count)
+int cuda_check(const char* where);
+int sm_count();
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+}  // namespace rkh
+
+#define RK_REQUIRE(cond, code, ...)      \
+  do {                                   \
+    if (!(cond)) {                       \
+      rkh::set_error(__VA_ARGS__);       \
+      return (code);                     \
+    }                                    \
+  } while (0)

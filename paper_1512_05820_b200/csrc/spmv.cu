@@ -1,0 +1,395 @@
+// K1 CSR SpMV (plain and fused into the PCG iteration), K2 SpMM, CSR diagonal and
+// symmetry validation.
+//
+// Replaces scipy csr_matvec / csr_matvecs behind linalg.spmv (linalg.py:138-148),
+// assemble_gram's A @ B (linalg.py:173), MatrixOperator.apply (krylov.py:56-57),
+// SparseSpdMatrix._validate (linalg.py:105-119) and JacobiPreconditioner's
+// diagonal (preconditioners.py:54-58).
+//
+// Layout: CSR with int32 indices, both triangles stored (as the reference).
+// A group of LANES consecutive lanes owns one row; each lane walks the row's
+// entries with stride LANES (coalesced within the group) and the group sums
+// with an xor butterfly. The matrix stream is loaded with ld.global.cs
+// (evict-first) so the gathered vector stays resident in L2.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace rk {
+
+constexpr int kSpmvThreads = 256;
+
+// Entries per lane per pass for each group width: LANES * U covers the
+// typical row in one pass (2 x 4 = 8 for 7-point rows, 16 x 6 = 96 for the
+// 81-entry Q1 elasticity rows).
+template <int LANES>
+struct RowUnroll {
+  static constexpr int U = (LANES == 8 || LANES == 16) ? 6 : 4;
+};
+
+template <int LANES>
+__device__ __forceinline__ double csr_row_dot(const int32_t* __restrict__ rp,
+                                              const int32_t* __restrict__ ci,
+                                              const double* __restrict__ val,
+                                              const double* __restrict__ x, int64_t row,
+                                              bool valid, int sub) {
+  // Each pass issues U independent (value, index) loads per lane before the
+  // dependent gathers, so a short row (81 entries at 32 lanes, 7 at 4 lanes)
+  // is a single pass with all its loads in flight at once.
+  constexpr int U = RowUnroll<LANES>::U;
+  double s = 0.0;
+  if (valid) {
+    const int32_t beg = __ldg(rp + row), end = __ldg(rp + row + 1);
+    for (int32_t j0 = beg + sub; j0 < end; j0 += LANES * U) {
+      double v[U];
+      int32_t c[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int32_t j = j0 + u * LANES;
+        const bool ok = j < end;
+        v[u] = ok ? __ldcs(val + j) : 0.0;
+        c[u] = ok ? __ldcs(ci + j) : 0;
+      }
+      double xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[u] = __ldg(x + c[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) s = fma(v[u], xv[u], s);
+    }
+  }
+#pragma unroll
+  for (int o = LANES / 2; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  return s;
+}
+
+template <int LANES>
+__global__ void __launch_bounds__(kSpmvThreads) k_spmv(int64_t n, const int32_t* __restrict__ rp,
+                                                       const int32_t* __restrict__ ci,
+                                                       const double* __restrict__ val,
+                                                       const double* __restrict__ x,
+                                                       double* __restrict__ y) {
+  constexpr int RPB = kSpmvThreads / LANES;
+  const int sub = threadIdx.x % LANES;
+  for (int64_t base = (int64_t)blockIdx.x * RPB; base < n; base += (int64_t)gridDim.x * RPB) {
+    const int64_t row = base + threadIdx.x / LANES;
+    const bool valid = row < n;
+    const double s = csr_row_dot<LANES>(rp, ci, val, x, row, valid, sub);
+    if (valid && sub == 0) y[row] = s;
+  }
+}
+
+// Breakdown test and step length of one iteration (krylov.py:302-305); run by
+// the single last block once gamma = p'Ap and p'p are known.
+__device__ __forceinline__ void curvature_epilogue(const rk_pcg_plan& P, double gamma, double pp) {
+  rk_pcg_state* st = P.st;
+  const int64_t k = st->k;
+  st->gamma = gamma;
+  st->pp = pp;
+  // krylov.py:303  `not isfinite(gamma) or gamma <= 1e-14 * (p @ p)`
+  if (!isfinite(gamma) || gamma <= 1e-14 * pp) {
+    st->status = 2;
+    st->bd_iter = k;
+    st->done = 1;
+    return;
+  }
+  const double alpha = st->rz / gamma;
+  st->alpha = alpha;
+  P.alpha_h[k] = alpha;
+  P.gamma_h[k] = gamma;
+  P.rz_h[k] = st->rz;
+}
+
+// K1 fused: Ap_k = A p_k with gamma = p'Ap and p'p reduced in the same pass.
+template <int LANES>
+__global__ void __launch_bounds__(kSpmvThreads) k_spmv_pcg(const rk_pcg_plan P) {
+  if (P.st->done) return;
+  constexpr int RPB = kSpmvThreads / LANES;
+  __shared__ double scratch[64];
+  const int64_t k = P.st->k;
+  const double* __restrict__ p = P.V + k * P.ldv;
+  double* __restrict__ Ap = P.AV + (P.ldav ? k * P.ldav : 0);
+  const int32_t* __restrict__ rp = P.A.rowptr;
+  const int32_t* __restrict__ ci = P.A.col;
+  const double* __restrict__ val = P.A.val;
+  const int64_t n = P.n;
+  const int sub = threadIdx.x % LANES;
+  double acc[2] = {0.0, 0.0};
+  for (int64_t base = (int64_t)blockIdx.x * RPB; base < n; base += (int64_t)gridDim.x * RPB) {
+    const int64_t row = base + threadIdx.x / LANES;
+    const bool valid = row < n;
+    const double s = csr_row_dot<LANES>(rp, ci, val, p, row, valid, sub);
+    if (valid && sub == 0) {
+      Ap[row] = s;
+      const double pr = p[row];
+      acc[0] = fma(pr, s, acc[0]);
+      acc[1] = fma(pr, pr, acc[1]);
+    }
+  }
+  block_sum<2>(acc, scratch);
+  if (publish_and_check_last(acc, 2, P.partials, P.tickets + 0)) {
+    __shared__ double tot[2];
+    combine_partials(P.partials, gridDim.x, 2, tot);
+    if (threadIdx.x == 0) curvature_epilogue(P, tot[0], tot[1]);
+  }
+}
+
+// Generic-operator variant: the caller already wrote A p_k; reduce gamma, p'p.
+__global__ void __launch_bounds__(kSpmvThreads) k_curvature(const rk_pcg_plan P) {
+  if (P.st->done) return;
+  __shared__ double scratch[64];
+  const int64_t k = P.st->k;
+  const double* __restrict__ p = P.V + k * P.ldv;
+  const double* __restrict__ Ap = P.AV + (P.ldav ? k * P.ldav : 0);
+  double acc[2] = {0.0, 0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P.n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double pr = p[i];
+    acc[0] = fma(pr, Ap[i], acc[0]);
+    acc[1] = fma(pr, pr, acc[1]);
+  }
+  block_sum<2>(acc, scratch);
+  if (publish_and_check_last(acc, 2, P.partials, P.tickets + 0)) {
+    __shared__ double tot[2];
+    combine_partials(P.partials, gridDim.x, 2, tot);
+    if (threadIdx.x == 0) curvature_epilogue(P, tot[0], tot[1]);
+  }
+}
+
+// K2 SpMM: Y[:, c0:c0+CT] = A X[:, c0:c0+CT]; the matrix row is read once per
+// column tile, the CT gathered columns share each (value, index) load.
+template <int LANES, int CT>
+__global__ void __launch_bounds__(kSpmvThreads) k_spmm(int64_t n, const int32_t* __restrict__ rp,
+                                                       const int32_t* __restrict__ ci,
+                                                       const double* __restrict__ val, int64_t m,
+                                                       const double* __restrict__ X, int64_t ldx,
+                                                       double* __restrict__ Y, int64_t ldy) {
+  constexpr int RPB = kSpmvThreads / LANES;
+  const int sub = threadIdx.x % LANES;
+  const int64_t c0 = (int64_t)blockIdx.y * CT;
+  const int ct = (int)min((int64_t)CT, m - c0);
+  for (int64_t base = (int64_t)blockIdx.x * RPB; base < n; base += (int64_t)gridDim.x * RPB) {
+    const int64_t row = base + threadIdx.x / LANES;
+    double acc[CT];
+#pragma unroll
+    for (int t = 0; t < CT; ++t) acc[t] = 0.0;
+    if (row < n) {
+      const int32_t beg = __ldg(rp + row), end = __ldg(rp + row + 1);
+      for (int32_t j = beg + sub; j < end; j += LANES) {
+        const double v = __ldg(val + j);
+        const double* xc = X + (int64_t)__ldg(ci + j) + c0 * ldx;
+#pragma unroll
+        for (int t = 0; t < CT; ++t)
+          if (t < ct) acc[t] = fma(v, __ldg(xc + t * ldx), acc[t]);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < CT; ++t) {
+#pragma unroll
+      for (int o = LANES / 2; o > 0; o >>= 1) acc[t] += __shfl_xor_sync(kFull, acc[t], o);
+    }
+    if (row < n && sub == 0) {
+#pragma unroll
+      for (int t = 0; t < CT; ++t)
+        if (t < ct) Y[row + (c0 + t) * ldy] = acc[t];
+    }
+  }
+}
+
+__global__ void k_csr_diagonal(int64_t n, const int32_t* __restrict__ rp,
+                               const int32_t* __restrict__ ci, const double* __restrict__ val,
+                               double* __restrict__ diag, double* __restrict__ dinv,
+                               unsigned long long* bad) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t lo = rp[i], hi = rp[i + 1] - 1;
+    double d = 0.0;
+    while (lo <= hi) {  // columns sorted: binary search for the diagonal
+      const int32_t mid = (lo + hi) >> 1;
+      const int32_t c = ci[mid];
+      if (c == i) { d = val[mid]; break; }
+      if (c < i) lo = mid + 1; else hi = mid - 1;
+    }
+    if (diag) diag[i] = d;
+    if (dinv) dinv[i] = 1.0 / d;  // preconditioners.py:58 `1.0 / diag` (IEEE division)
+    if (!(d > 0.0)) atomicMin(bad, (unsigned long long)i);
+  }
+}
+
+// max |A_ij - A_ji| over stored entries (missing transpose entries count as 0)
+// and max |A_ij|; max is order independent, so this is deterministic.
+__global__ void __launch_bounds__(256) k_csr_asymmetry(int64_t n, const int32_t* __restrict__ rp,
+                                                       const int32_t* __restrict__ ci,
+                                                       const double* __restrict__ val,
+                                                       double* partials, uint32_t* ticket,
+                                                       double* out2) {
+  double worst = 0.0, scale = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    for (int32_t e = rp[i]; e < rp[i + 1]; ++e) {
+      const int32_t j = ci[e];
+      const double v = val[e];
+      scale = fmax(scale, fabs(v));
+      int32_t lo = rp[j], hi = rp[j + 1] - 1;
+      double vt = 0.0;
+      while (lo <= hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        const int32_t c = ci[mid];
+        if (c == i) { vt = val[mid]; break; }
+        if (c < i) lo = mid + 1; else hi = mid - 1;
+      }
+      worst = fmax(worst, fabs(v - vt));
+    }
+  }
+  __shared__ double sw[32], ss[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    worst = fmax(worst, __shfl_xor_sync(kFull, worst, o));
+    scale = fmax(scale, __shfl_xor_sync(kFull, scale, o));
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (lane == 0) { sw[warp] = worst; ss[warp] = scale; }
+  __syncthreads();
+  double v2[2] = {0.0, 0.0};
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < nw; ++w) { v2[0] = fmax(v2[0], sw[w]); v2[1] = fmax(v2[1], ss[w]); }
+  }
+  __shared__ double vs[2];
+  if (threadIdx.x == 0) { vs[0] = v2[0]; vs[1] = v2[1]; }
+  __syncthreads();
+  if (publish_and_check_last(vs, 2, partials, ticket)) {
+    if (threadIdx.x == 0) {
+      double a = 0.0, b = 0.0;
+      for (unsigned blk = 0; blk < gridDim.x; ++blk) {
+        a = fmax(a, __ldcg(partials + 2 * blk));
+        b = fmax(b, __ldcg(partials + 2 * blk + 1));
+      }
+      out2[0] = a;
+      out2[1] = b;
+    }
+  }
+}
+
+}  // namespace rk
+
+// ---------------------------------------------------------------------------
+// Launchers
+// ---------------------------------------------------------------------------
+namespace rkh {
+
+int auto_lanes(const rk_csr& A) {
+  if (A.lanes > 0) return A.lanes;
+  const double avg = A.n > 0 ? (double)A.nnz / (double)A.n : 1.0;
+  if (avg <= 3.0) return 1;
+  if (avg <= 7.5) return 2;
+  if (avg <= 14.0) return 4;
+  if (avg <= 44.0) return 8;
+  if (avg <= 90.0) return 16;
+  return 32;
+}
+
+int spmv_grid(int64_t n, int lanes) {
+  const int64_t rpb = rk::kSpmvThreads / lanes;
+  const int64_t need = (n + rpb - 1) / rpb;
+  const int64_t cap = (int64_t)sm_count() * 8;
+  return (int)std::max<int64_t>(1, std::min(need, cap));
+}
+
+// One resident wave: grid = (resident blocks per SM) x SMs, rows grid-strided.
+template <typename Kern>
+static int resident_grid(Kern kern, int threads, int64_t need) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, 0) != cudaSuccess || occ < 1) occ = 1;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)occ * sm_count()));
+}
+
+template <int L>
+static void launch_spmv_l(const rk_csr& A, const double* x, double* y, cudaStream_t s) {
+  static const int cap = resident_grid(rk::k_spmv<L>, rk::kSpmvThreads, INT64_MAX);
+  const int grid = (int)std::min<int64_t>(cap, (A.n + rk::kSpmvThreads / L - 1) / (rk::kSpmvThreads / L));
+  rk::k_spmv<L><<<std::max(grid, 1), rk::kSpmvThreads, 0, s>>>(A.n, A.rowptr, A.col, A.val, x, y); rkh::note_launch();
+}
+
+int launch_spmv(const rk_csr& A, const double* x, double* y, cudaStream_t s) {
+  switch (auto_lanes(A)) {
+    case 1: launch_spmv_l<1>(A, x, y, s); break;
+    case 2: launch_spmv_l<2>(A, x, y, s); break;
+    case 4: launch_spmv_l<4>(A, x, y, s); break;
+    case 8: launch_spmv_l<8>(A, x, y, s); break;
+    case 16: launch_spmv_l<16>(A, x, y, s); break;
+    default: launch_spmv_l<32>(A, x, y, s); break;
+  }
+  return cuda_check("rk_spmv");
+}
+
+template <int L>
+static void launch_spmv_pcg_l(const rk_pcg_plan& P, cudaStream_t s) {
+  static const int cap = std::min(resident_grid(rk::k_spmv_pcg<L>, rk::kSpmvThreads, INT64_MAX), sm_count() * 8);
+  const int grid = (int)std::min<int64_t>(cap, (P.n + rk::kSpmvThreads / L - 1) / (rk::kSpmvThreads / L));
+  rk::k_spmv_pcg<L><<<std::max(grid, 1), rk::kSpmvThreads, 0, s>>>(P); rkh::note_launch();
+}
+
+void launch_spmv_pcg(const rk_pcg_plan& P, cudaStream_t s) {
+  switch (auto_lanes(P.A)) {
+    case 1: launch_spmv_pcg_l<1>(P, s); break;
+    case 2: launch_spmv_pcg_l<2>(P, s); break;
+    case 4: launch_spmv_pcg_l<4>(P, s); break;
+    case 8: launch_spmv_pcg_l<8>(P, s); break;
+    case 16: launch_spmv_pcg_l<16>(P, s); break;
+    default: launch_spmv_pcg_l<32>(P, s); break;
+  }
+}
+
+int curvature_grid(int64_t n) {
+  const int64_t need = (n + 255) / 256;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sm_count() * 4));
+}
+
+void launch_curvature(const rk_pcg_plan& P, cudaStream_t s) {
+  rk::k_curvature<<<curvature_grid(P.n), 256, 0, s>>>(P); rkh::note_launch();
+}
+
+template <int L>
+static void launch_spmm_l(const rk_csr& A, int64_t m, const double* X, int64_t ldx, double* Y,
+                          int64_t ldy, cudaStream_t s) {
+  constexpr int CT = 8;
+  const int64_t tiles = (m + CT - 1) / CT;
+  const int64_t rpb = rk::kSpmvThreads / L;
+  int64_t gx = (A.n + rpb - 1) / rpb;
+  gx = std::max<int64_t>(1, std::min<int64_t>(gx, std::max<int64_t>(1, (int64_t)sm_count() * 8 / std::max<int64_t>(1, std::min<int64_t>(tiles, 8)))));
+  dim3 grid((unsigned)gx, (unsigned)tiles);
+  rk::k_spmm<L, CT><<<grid, rk::kSpmvThreads, 0, s>>>(A.n, A.rowptr, A.col, A.val, m, X, ldx, Y, ldy); rkh::note_launch();
+}
+
+int launch_spmm(const rk_csr& A, int64_t m, const double* X, int64_t ldx, double* Y, int64_t ldy,
+                cudaStream_t s) {
+  if (m <= 0 || A.n <= 0) return 0;
+  switch (auto_lanes(A)) {
+    case 1: launch_spmm_l<1>(A, m, X, ldx, Y, ldy, s); break;
+    case 2: launch_spmm_l<2>(A, m, X, ldx, Y, ldy, s); break;
+    case 4: launch_spmm_l<4>(A, m, X, ldx, Y, ldy, s); break;
+    case 8: launch_spmm_l<8>(A, m, X, ldx, Y, ldy, s); break;
+    case 16: launch_spmm_l<16>(A, m, X, ldx, Y, ldy, s); break;
+    default: launch_spmm_l<32>(A, m, X, ldx, Y, ldy, s); break;
+  }
+  return cuda_check("rk_spmm");
+}
+
+int launch_csr_diagonal(const rk_csr& A, double* diag, double* dinv, int64_t* bad, cudaStream_t s) {
+  if (cudaMemsetAsync(bad, 0xff, sizeof(int64_t), s) != cudaSuccess) return cuda_check("rk_csr_diagonal");
+  if (A.n > 0) {
+    const int grid = curvature_grid(A.n);
+    rk::k_csr_diagonal<<<grid, 256, 0, s>>>(A.n, A.rowptr, A.col, A.val, diag, dinv,
+                                            reinterpret_cast<unsigned long long*>(bad)); rkh::note_launch();
+  }
+  return cuda_check("rk_csr_diagonal");
+}
+
+int launch_csr_asymmetry(const rk_csr& A, double* out2, double* ws, int64_t ws_len, uint32_t* tickets,
+                         cudaStream_t s) {
+  const int grid = curvature_grid(std::max<int64_t>(A.n, 1));
+  RK_REQUIRE(ws_len >= 2 * grid, RK_ERR_ARG, "rk_csr_asymmetry: workspace too small (%lld < %d)",
+             (long long)ws_len, 2 * grid);
+  rk::k_csr_asymmetry<<<grid, 256, 0, s>>>(A.n, A.rowptr, A.col, A.val, ws, tickets, out2); rkh::note_launch();
+  return cuda_check("rk_csr_asymmetry");
+}
+
+}  // namespace rkh

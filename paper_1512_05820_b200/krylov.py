@@ -1,0 +1,628 @@
+"""Augmented preconditioned CG on the device (``recykl/krylov.py``).
+
+Same public surface as the reference: ``LinearOperator`` (krylov.py:39-45),
+``MatrixOperator`` (48-57), ``ReducedSpdOperator`` (60-83),
+``BlockDiagFactor`` (97-132), ``DirectReducedProjection`` (135-156),
+``AugmentedPcgResult`` (159-178), ``augmented_pcg`` (181-345), ``pcg``
+(348-386), ``direct_reduced_solve`` (396-411).
+
+Two drivers run the same kernels:
+
+* the fused path (CSR operator, Jacobi/identity/no preconditioner, no
+  monitor, direct projection): every iteration is launched from C
+  (``rk_pcg_steps``) in batches; convergence, breakdown and the step scalars
+  live in device memory and the host reads the 96-byte state once per batch;
+* the stepped path (any ``LinearOperator``, a callable reduced solver, or a
+  monitor): the same update/direction kernels, one host synchronisation per
+  iteration so Python callbacks can run in between.
+
+Directions are written straight into the column-major block V (column k is
+p_k), so the result's ``V`` needs no ``column_stack`` (krylov.py:273).
+Returned ``x`` and ``V`` are device tensors; ``vhat``, ``gamma`` and
+``residual_history`` are small host arrays, as in the reference.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .errors import Breakdown, DimensionMismatch, NotConverged
+from .linalg import (
+    F64,
+    DenseLowerTriangular,
+    InstrumentationSink,
+    SparseSpdMatrix,
+    as_block,
+    as_matrix,
+    as_vector,
+    block_ld,
+    dense_cholesky,
+    empty_block,
+    gemv_n,
+    gemv_t,
+    gram,
+    norm,
+    spmm,
+    spmv,
+    spmv_into,
+    to_numpy,
+)
+from .preconditioners import IdentityPreconditioner, JacobiPreconditioner
+
+_BREAKDOWN_RTOL = 1e-14  # krylov.py:36 (applied on the device, spmv.cu)
+
+
+class LinearOperator:
+    """SPD operator on R^dim acting on device vectors."""
+
+    dim: int
+    device: torch.device
+
+    def apply(self, x) -> torch.Tensor:
+        raise NotImplementedError
+
+
+class MatrixOperator(LinearOperator):
+    """A device CSR matrix as an operator, charging a shared sink."""
+
+    def __init__(self, A, sink: InstrumentationSink | None = None):
+        self.A = as_matrix(A)
+        self.sink = sink
+        self.dim = self.A.n
+        self.device = self.A.device
+
+    def apply(self, x):
+        return spmv(self.A, x, self.sink)
+
+
+class ReducedSpdOperator(LinearOperator):
+    """p -> Y'(A(Yp)) without forming Y'AY (krylov.py:60-83): GEMV-N, SpMV,
+    GEMV-T on the device. With ``record_products`` the full-space products
+    A(Yp) are kept (as columns of one device block) for later stages."""
+
+    def __init__(self, A, Y, sink=None, record_products: bool = False):
+        self.A = as_matrix(A)
+        self.device = self.A.device
+        self.Y = as_block(Y, self.device)
+        self.sink = sink
+        self.dim = int(self.Y.shape[1])
+        self._record = record_products
+        self._full = None
+        self._count = 0
+        self.reduced_products: list | None = [] if record_products else None
+
+    def apply(self, p):
+        pd = as_vector(p, self.device)
+        full = spmv(self.A, gemv_n(self.Y, pd), self.sink)
+        reduced = gemv_t(self.Y, full)
+        if self._record:
+            if self._full is None or self._count >= self._full.shape[1]:
+                cap = max(16, 2 * self._count)
+                grown = empty_block(self.A.n, cap, self.device)
+                if self._count:
+                    grown[:, : self._count].copy_(self._full[:, : self._count])
+                self._full = grown
+            self._full[:, self._count].copy_(full)
+            self._count += 1
+            self.reduced_products.append(reduced)
+        return reduced
+
+    @property
+    def full_products(self):
+        if not self._record:
+            return None
+        return [self._full[:, i] for i in range(self._count)]
+
+    def full_products_block(self, count: int | None = None) -> torch.Tensor:
+        """Column-stacked A(Y p_i) for the first ``count`` applications."""
+        c = self._count if count is None else int(count)
+        if c == 0 or self._full is None:
+            return empty_block(self.A.n, 0, self.device)
+        return self._full[:, :c]
+
+
+def _as_operator(op, sink):
+    if isinstance(op, LinearOperator):
+        return op
+    if isinstance(op, SparseSpdMatrix):
+        return MatrixOperator(op, sink)
+    if hasattr(op, "row_offsets") or hasattr(op, "tocsr"):
+        return MatrixOperator(SparseSpdMatrix.from_host(op), sink)
+    arr = to_numpy(op) if isinstance(op, torch.Tensor) else np.asarray(op, dtype=np.float64)
+    if arr.ndim == 2 and arr.shape[0] == arr.shape[1]:
+        return MatrixOperator(SparseSpdMatrix.from_dense(arr), sink)
+    raise DimensionMismatch("unsupported operator type")
+
+
+class BlockDiagFactor:
+    """Cholesky factor of a block-diagonal Gram matrix (krylov.py:97-132):
+    dense lower-triangular blocks or square roots of diagonal blocks."""
+
+    def __init__(self):
+        self._blocks: list = []
+        self.size = 0
+        self._dev = {}
+
+    def append_cholesky(self, factor: DenseLowerTriangular):
+        self._blocks.append(("chol", factor))
+        self.size += factor.m
+        self._dev.clear()
+
+    def append_sqrt_diag(self, sqrt_diag):
+        sd = np.asarray(to_numpy(sqrt_diag), dtype=np.float64)
+        self._blocks.append(("sqrtdiag", sd))
+        self.size += sd.shape[0]
+        self._dev.clear()
+
+    def solve_spd(self, rhs):
+        rhs = np.asarray(to_numpy(rhs), dtype=np.float64)
+        if rhs.shape[0] != self.size:
+            raise DimensionMismatch("block factor: rhs length mismatch")
+        out = np.empty_like(rhs)
+        at = 0
+        for kind, block in self._blocks:
+            if kind == "chol":
+                m = block.m
+                out[at : at + m] = block.solve_spd(rhs[at : at + m])
+            else:
+                m = block.shape[0]
+                out[at : at + m] = rhs[at : at + m] / (block * block)
+            at += m
+        return out
+
+    def device_form(self, device):
+        """(L, wchol, sqd) for the fused kernels: one leading dense block and a
+        trailing sqrt-diagonal; other block patterns are densified."""
+        key = (device.type, device.index)
+        hit = self._dev.get(key)
+        if hit is not None:
+            return hit
+        kinds = [k for k, _ in self._blocks]
+        if all(k == "sqrtdiag" for k in kinds[1:]) and (not kinds or kinds[0] in ("chol", "sqrtdiag")):
+            if kinds and kinds[0] == "chol":
+                L = self._blocks[0][1]
+                w = L.m
+                Ld = L.device(device)
+                rest = [b for _, b in self._blocks[1:]]
+            else:
+                w, Ld = 0, None
+                rest = [b for _, b in self._blocks]
+            sqd = np.concatenate(rest) if rest else np.zeros(0)
+            sqd_d = torch.from_numpy(np.ascontiguousarray(sqd)).to(device) if sqd.size else None
+            out = (Ld, w, sqd_d)
+        else:
+            Lfull = np.zeros((self.size, self.size))
+            at = 0
+            for kind, block in self._blocks:
+                if kind == "chol":
+                    Lfull[at : at + block.m, at : at + block.m] = block.full()
+                    at += block.m
+                else:
+                    m = block.shape[0]
+                    Lfull[np.arange(at, at + m), np.arange(at, at + m)] = block
+                    at += m
+            out = (as_block(Lfull, device), self.size, None)
+        self._dev[key] = out
+        return out
+
+
+class DirectReducedProjection:
+    """mu = (B'AB)^{-1} B'Az from the cached product cross = A B
+    (krylov.py:135-156). Inside the fused PCG kernels the GEMV-T and the
+    factor solve run on the device; called directly it returns mu (host)."""
+
+    def __init__(self, cross, factor):
+        self.cross = as_block(cross)
+        self.factor = factor
+
+    @classmethod
+    def assemble(cls, op, B) -> "DirectReducedProjection":
+        """A*B with m operator applications (charged m matvecs, no gram) and a
+        Cholesky of B'AB (krylov.py:147-153)."""
+        Bd = as_block(B, getattr(op, "device", None))
+        m = int(Bd.shape[1])
+        if isinstance(op, MatrixOperator):
+            cross = spmm(op.A, Bd)
+            if op.sink is not None:
+                op.sink.add_matvec(m)
+        else:
+            cross = empty_block(Bd.shape[0], m, Bd.device)
+            for i in range(m):
+                cross[:, i].copy_(op.apply(Bd[:, i]))
+        g = to_numpy(gram(Bd, cross))
+        return cls(cross, dense_cholesky(0.5 * (g + g.T)))
+
+    def __call__(self, z):
+        zd = as_vector(z, self.cross.device)
+        return self.factor.solve_spd(to_numpy(gemv_t(self.cross, zd)))
+
+
+@dataclass
+class AugmentedPcgResult:
+    """Outputs of one augmented-PCG run (krylov.py:159-178); ``x`` and ``V``
+    are device tensors in the run's own coordinates."""
+
+    k: int
+    vhat: np.ndarray
+    V: torch.Tensor
+    gamma: np.ndarray
+    residual_history: np.ndarray
+    x: torch.Tensor
+    converged: bool = True
+
+    @property
+    def final_residual(self) -> float:
+        return float(self.residual_history[-1])
+
+
+# ---------------------------------------------------------------------------
+# device run buffers
+# ---------------------------------------------------------------------------
+class _Run:
+    """Buffers and the rk_pcg_plan of one augmented-PCG run."""
+
+    def __init__(self, n, device, mode_code, keep_av, m, vcap):
+        self.n, self.device, self.mode_code, self.keep_av, self.m = n, device, mode_code, keep_av, m
+        self.x = torch.zeros(n, dtype=F64, device=device)
+        self.r = torch.empty(n, dtype=F64, device=device)
+        self.z = torch.empty(n, dtype=F64, device=device)
+        self.mu = torch.zeros(max(m, 1), dtype=F64, device=device)
+        self.st = torch.zeros(nat.STATE_BYTES, dtype=torch.uint8, device=device)
+        self.tickets = torch.zeros(16, dtype=torch.int32, device=device)
+        self.st_host = torch.empty(nat.STATE_BYTES, dtype=torch.uint8, pin_memory=True)
+        self.cstate = nat.RkPcgState.from_buffer(self.st_host.numpy())
+        self.vcap = 0
+        self.V = self.AV = self.ap = None
+        self._alloc(vcap)
+        self.plan = nat.RkPcgPlan()
+        self._fill_plan()
+
+    def _alloc(self, vcap):
+        n, dev = self.n, self.device
+        old = self.vcap
+        V = empty_block(n, vcap, dev)
+        AV = empty_block(n, vcap, dev) if self.keep_av else None
+        hist = torch.zeros((4, vcap + 1), dtype=F64, device=dev)
+        if old:
+            V[:, :old].copy_(self.V)
+            if self.keep_av:
+                AV[:, :old].copy_(self.AV)
+            hist[:, : old + 1].copy_(self.hist)
+        self.V, self.AV, self.hist = V, AV, hist
+        if not self.keep_av and self.ap is None:
+            self.ap = torch.empty(n, dtype=F64, device=dev)
+        self.coef = torch.empty(vcap + 1, dtype=F64, device=dev)
+        need = nat.lib().rk_pcg_workspace_doubles(n, self.m, vcap)
+        self.ws = torch.empty(max(need, 1), dtype=F64, device=dev)
+        self.vcap = vcap
+
+    def ensure(self, cols):
+        if cols > self.vcap:
+            self._alloc(max(cols, 2 * self.vcap))
+            self._fill_plan()
+
+    def _fill_plan(self):
+        P = self.plan
+        P.n = self.n
+        P.x, P.r, P.z = self.x.data_ptr(), self.r.data_ptr(), self.z.data_ptr()
+        P.V, P.ldv, P.vcap = self.V.data_ptr(), block_ld(self.V), self.vcap
+        if self.keep_av:
+            P.AV, P.ldav = self.AV.data_ptr(), block_ld(self.AV)
+        else:
+            P.AV, P.ldav = self.ap.data_ptr(), 0
+        P.mu, P.coef, P.st = self.mu.data_ptr(), self.coef.data_ptr(), self.st.data_ptr()
+        h = self.hist
+        P.alpha_h, P.gamma_h, P.rz_h, P.res_h = (h[i].data_ptr() for i in range(4))
+        P.partials, P.partials_len, P.tickets = self.ws.data_ptr(), self.ws.numel(), self.tickets.data_ptr()
+        P.mode = self.mode_code
+
+    def set_projection(self, B, cross, factor_dev):
+        P = self.plan
+        if B is None:
+            P.m, P.B, P.ldb, P.cross, P.ldc, P.L, P.ldl, P.wchol, P.sqd = 0, None, 0, None, 0, None, 0, 0, None
+            return
+        self._keep = (B, cross, factor_dev)
+        L, w, sqd = factor_dev
+        P.m = int(B.shape[1])
+        P.B, P.ldb = B.data_ptr(), block_ld(B)
+        P.cross, P.ldc = cross.data_ptr(), block_ld(cross)
+        P.L, P.ldl, P.wchol = (L.data_ptr(), block_ld(L), w) if L is not None and w else (None, 0, 0)
+        P.sqd = sqd.data_ptr() if sqd is not None else None
+
+    def set_csr(self, A: SparseSpdMatrix | None):
+        self.plan.A = A.csr if A is not None else nat.RkCsr()
+
+    def set_precond(self, dinv):
+        self.plan.dinv = dinv.data_ptr() if dinv is not None else None
+
+    def write_state(self, threshold):
+        ctypes_zero(self.cstate)
+        self.cstate.threshold = float(threshold)
+        self.st.copy_(self.st_host)
+
+    def read_state(self):
+        self.st_host.copy_(self.st)  # synchronising D2H of 96 bytes
+        return self.cstate
+
+    def histories(self, k):
+        h = to_numpy(self.hist[:, : k + 1])
+        return h[0, :k].copy(), h[1, :k].copy(), h[3, : k + 1].copy()
+
+    def ap_column(self, k):
+        return self.AV[:, k] if self.keep_av else self.ap
+
+
+def ctypes_zero(s):
+    import ctypes
+
+    ctypes.memset(ctypes.addressof(s), 0, ctypes.sizeof(s))
+
+
+_MODES = {"cg": 0, "fom": 1}
+
+
+def augmented_pcg(
+    op,
+    b,
+    yhat0=None,
+    aug_basis=None,
+    reduced_solver=None,
+    precond=None,
+    tol: float = 0.0,
+    *,
+    mode: str = "cg",
+    paper_fom_beta: bool = False,
+    relative: bool = False,
+    max_iter: int | None = None,
+    sink: InstrumentationSink | None = None,
+    r0=None,
+    monitor=None,
+    batch: int | None = None,
+) -> AugmentedPcgResult:
+    """Augmented PCG over the affine space Y yhat0 + directions (krylov.py:181-345).
+
+    Same parameters, exceptions (``NotConverged`` with the partial result,
+    ``Breakdown``, ``DimensionMismatch``, ``ValueError`` for an unknown mode)
+    and sink accounting as the reference. ``batch`` caps the number of
+    iterations launched between host checks on the fused path.
+    """
+    operator = _as_operator(op, sink)
+    n = int(operator.dim)
+    device = operator.device
+    bd = as_vector(b, device)
+    if bd.shape[0] != n:
+        raise DimensionMismatch("augmented_pcg: rhs length mismatch")
+
+    Y = None
+    if aug_basis is not None:
+        if isinstance(aug_basis, torch.Tensor):
+            if aug_basis.dim() != 2 or aug_basis.shape[0] != n:
+                raise DimensionMismatch("augmented_pcg: basis shape mismatch")
+        else:
+            arr = np.asarray(aug_basis)
+            if arr.ndim != 2 or arr.shape[0] != n:
+                raise DimensionMismatch("augmented_pcg: basis shape mismatch")
+        Y = as_block(aug_basis, device)
+        if Y.shape[1] == 0:
+            Y = None
+    if Y is not None:
+        if yhat0 is None:
+            raise DimensionMismatch("augmented_pcg: yhat0 required with a nonempty basis")
+        yh = as_vector(yhat0, device)
+        if yh.shape[0] != Y.shape[1]:
+            raise DimensionMismatch("augmented_pcg: yhat0 length mismatch")
+        if reduced_solver is None:
+            reduced_solver = DirectReducedProjection.assemble(operator, Y)
+
+    code = _MODES.get(mode, -1)
+    if code == 1 and paper_fom_beta:
+        code = 2
+    direct = isinstance(reduced_solver, DirectReducedProjection)
+    m = int(Y.shape[1]) if Y is not None else 0
+    keep_av = code == 1
+    max_iter = n if max_iter is None else int(max_iter)
+    run = _Run(n, device, max(code, 0), keep_av, m if direct else 0, vcap=min(max_iter + 2, 64))
+
+    if Y is not None:
+        gemv_n(Y, yh, out=run.x)
+    if r0 is not None:
+        r0d = as_vector(r0, device)
+        if r0d.shape[0] != n:
+            raise DimensionMismatch("augmented_pcg: r0 length mismatch")
+        run.r.copy_(r0d)
+    elif Y is not None and bool(torch.any(run.x != 0)):
+        run.r.copy_(bd - operator.apply(run.x))
+    else:
+        run.r.copy_(bd)
+    threshold = tol * norm(bd) if relative else tol
+
+    if precond is None:
+        dinv = None
+    elif isinstance(precond, (JacobiPreconditioner, IdentityPreconditioner)):
+        dinv = precond.fused_inverse_diagonal()
+    else:
+        raise NotImplementedError(f"preconditioner {getattr(precond, 'kind', precond)!r} has no device form")
+    run.set_precond(dinv)
+    run.set_csr(operator.A if isinstance(operator, MatrixOperator) else None)
+    if direct:
+        run.set_projection(Y, reduced_solver.cross, reduced_solver.factor.device_form(device))
+    else:
+        run.set_projection(None, None, None)
+
+    run.write_state(threshold)
+    # entry: z = M^{-1} r, ||r0||, rz, mu, p_0 (krylov.py:268,290-292)
+    nat.check(nat.lib().rk_pcg_entry(run.plan, nat.stream_ptr(device)), "augmented_pcg entry")
+    run.read_state()
+    res0 = float(run.hist[3, 0].cpu())
+    if monitor is not None:
+        monitor(0, run.x.clone())
+    if res0 <= threshold:  # krylov.py:284-285
+        return _result(run, 0, True)
+    if precond is not None and sink is not None:
+        sink.add_precond()
+    if Y is not None and not direct:
+        _direction_with_callback(run, Y, reduced_solver, entry=True)
+    if code < 0:
+        # the reference raises at the first direction update (krylov.py:338-339)
+        _count_matvecs(operator, 1)
+        raise ValueError(f"unknown mode {mode!r}")
+
+    fused = isinstance(operator, MatrixOperator) and (Y is None or direct) and monitor is None
+    if fused:
+        k_final, status = _drive_fused(run, max_iter, batch)
+    else:
+        k_final, status = _drive_stepped(run, operator, Y, reduced_solver, direct, max_iter, monitor)
+
+    # cost accounting identical to the reference's call pattern; the stepped
+    # driver charges its operator applications as they happen
+    if status == 2:
+        bd_iter = int(run.cstate.bd_iter)
+        if fused:
+            _count_matvecs(operator, bd_iter + 1)
+        if precond is not None and sink is not None:
+            sink.add_precond(bd_iter)
+        raise Breakdown(f"direction curvature {run.cstate.gamma:.3e} at iteration {bd_iter}")
+    if fused:
+        _count_matvecs(operator, k_final)
+    if status == 1:
+        if precond is not None and sink is not None:
+            sink.add_precond(k_final - 1)
+        return _result(run, k_final, True)
+    if precond is not None and sink is not None:
+        sink.add_precond(max_iter)
+    raise NotConverged(
+        f"no convergence to {threshold:.3e} within {max_iter} iterations",
+        partial=_result(run, max_iter, False),
+    )
+
+
+def _count_matvecs(operator, count):
+    if isinstance(operator, MatrixOperator) and operator.sink is not None and count:
+        operator.sink.add_matvec(count)
+
+
+def _result(run: _Run, k: int, converged: bool) -> AugmentedPcgResult:
+    alphas, gammas, hist = run.histories(k)
+    return AugmentedPcgResult(
+        k=k, vhat=alphas, V=run.V[:, :k], gamma=gammas, residual_history=hist, x=run.x, converged=converged
+    )
+
+
+def _drive_fused(run: _Run, max_iter: int, batch: int | None):
+    """Batched device iterations; one 96-byte state read per batch."""
+    launched = 0
+    step = 4
+    cap = int(batch) if batch else 64
+    st = run.cstate
+    while launched < max_iter:
+        nb = min(step, cap, max_iter - launched)
+        run.ensure(launched + nb + 1)
+        nat.check(nat.lib().rk_pcg_steps(run.plan, nb, launched + nb - 1, nat.stream_ptr(run.device)),
+                  "augmented_pcg steps")
+        launched += nb
+        st = run.read_state()
+        if st.done:
+            return int(st.k), int(st.status)
+        step = min(step * 2, cap)
+    return int(st.k), int(st.status)
+
+
+def _direction_with_callback(run: _Run, Y, reduced_solver, entry: bool):
+    """mu from a Python reduced solver (e.g. the nested phi=1 projection), then
+    the direction kernel with that mu (krylov.py:291,322-326)."""
+    mu = as_vector(reduced_solver(run.z), run.device)
+    P = run.plan
+    saved = (P.m, P.B, P.ldb, P.mu)
+    P.m, P.B, P.ldb, P.mu = int(Y.shape[1]), Y.data_ptr(), block_ld(Y), mu.data_ptr()
+    try:
+        if entry:  # p_0 = z - Y mu (the entry kernel wrote p_0 = z)
+            nat.check(nat.lib().rk_gemv_n(run.n, P.m, P.B, P.ldb, P.mu, run.z.data_ptr(), run.V.data_ptr(), 2,
+                                          nat.stream_ptr(run.device)), "entry direction")
+        else:
+            nat.check(nat.lib().rk_pcg_direction(P, int(run.cstate.k), nat.stream_ptr(run.device)),
+                      "augmented_pcg direction")
+    finally:
+        P.m, P.B, P.ldb, P.mu = saved
+        del mu
+
+
+def _drive_stepped(run: _Run, operator, Y, reduced_solver, direct, max_iter, monitor):
+    """One iteration at a time: operator callback, curvature, update, direction."""
+    dev = run.device
+    st = run.cstate
+    for it in range(max_iter):
+        run.ensure(it + 2)
+        k = it
+        p = run.V[:, k]
+        dst = run.ap_column(k)
+        if isinstance(operator, MatrixOperator):
+            spmv_into(operator.A, p, dst)
+            _count_matvecs(operator, 1)
+        else:
+            dst.copy_(as_vector(operator.apply(p), dev))
+        nat.check(nat.lib().rk_pcg_curvature(run.plan, nat.stream_ptr(dev)), "curvature")
+        nat.check(nat.lib().rk_pcg_update(run.plan, nat.stream_ptr(dev)), "update")
+        st = run.read_state()
+        if st.status == 2:
+            return int(st.k), 2
+        if monitor is not None:
+            monitor(k + 1, run.x.clone())
+        if st.done:
+            return int(st.k), int(st.status)
+        if Y is not None and not direct:
+            _direction_with_callback(run, Y, reduced_solver, entry=False)
+        else:
+            nat.check(nat.lib().rk_pcg_direction(run.plan, k, nat.stream_ptr(dev)), "direction")
+    st = run.read_state()
+    return int(st.k), int(st.status)
+
+
+def pcg(A, b, x0=None, precond=None, tol: float = 0.0, max_iter: int | None = None, *, mode: str = "cg",
+        relative: bool = False, sink: InstrumentationSink | None = None, monitor=None) -> AugmentedPcgResult:
+    """Plain PCG, the empty-basis case of augmented_pcg (krylov.py:348-386)."""
+    operator = _as_operator(A, sink)
+    bd = as_vector(b, operator.device)
+    shift = None
+    rhs = bd
+    if x0 is not None:
+        x0d = as_vector(x0, operator.device)
+        if bool(torch.any(x0d != 0)):
+            rhs = bd - operator.apply(x0d)
+            shift = x0d
+    try:
+        res = augmented_pcg(operator, rhs, precond=precond, tol=tol, max_iter=max_iter, mode=mode,
+                            relative=relative, sink=sink, monitor=monitor)
+    except NotConverged as exc:
+        if shift is not None and exc.partial is not None:
+            exc.partial.x = exc.partial.x + shift
+        raise
+    if shift is not None:
+        res.x = res.x + shift
+    return res
+
+
+@dataclass
+class DirectSolveResult:
+    what: np.ndarray
+    rhat: DenseLowerTriangular
+    aw: torch.Tensor  # cached A @ W on the device
+
+
+def direct_reduced_solve(A, b, W, sink: InstrumentationSink | None = None) -> DirectSolveResult:
+    """Galerkin solve over range(W) by Cholesky of W'AW (krylov.py:396-411):
+    SpMM + DMMA Gram on the device, dpotrf and the two triangular solves on
+    the host (w x w)."""
+    from .linalg import assemble_gram
+
+    A = as_matrix(A)
+    Wd = as_block(W, A.device)
+    bd = as_vector(b, A.device)
+    G, AW = assemble_gram(A, Wd, sink)
+    g = to_numpy(G)
+    rhat = dense_cholesky(0.5 * (g + g.T))
+    what = rhat.solve_spd(to_numpy(gemv_t(Wd, bd)))
+    return DirectSolveResult(what=what, rhat=rhat, aw=AW)

@@ -1,0 +1,655 @@
+"""Device-resident sparse and dense kernels behind the reference's ``linalg`` API.
+
+Mirrors ``recykl/linalg.py``: ``InstrumentationSink`` (linalg.py:29-60),
+``SparseSpdMatrix`` (63-135), ``spmv`` (138-148), ``weighted_inner`` (151-157),
+``assemble_gram`` (160-174), ``DenseBasis`` (177-205),
+``DenseLowerTriangular`` (217-247), ``dense_cholesky`` (250-267),
+``symmetric_evd`` (270-280), ``thin_svd`` (283-290),
+``principal_angle_distance`` (319-337).
+
+Vectors and N x m blocks live on the GPU as float64 torch tensors; blocks are
+column-major (``stride(0) == 1``) with a leading dimension padded to a
+multiple of 32 rows so every column is 256-byte aligned. The small dense
+factorizations (Cholesky of w x w, eigh of m x m) run on the host through the
+same LAPACK routines the reference calls (dpotrf, dsyevd), which keeps the
+reduced problems bit-compatible with the oracle; everything of size N runs in
+``libpodcg.so``.
+"""
+
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.linalg
+import scipy.sparse
+import torch
+
+from . import _native as nat
+from .errors import DimensionMismatch, IterationLimit, NotPositiveDefinite, NotSymmetric, RankDeficient
+
+_SYMMETRY_RTOL = 1e-12
+LD_ALIGN = 32
+F64 = torch.float64
+
+
+class InstrumentationSink:
+    """Lock-protected cost counters, same semantics as linalg.py:29-60."""
+
+    def __init__(self):
+        self._lock = threading.Lock()
+        self.matvecs = 0
+        self.precond_applies = 0
+        self.gram_assemblies = 0
+
+    def add_matvec(self, count: int = 1) -> None:
+        with self._lock:
+            self.matvecs += count
+
+    def add_precond(self, count: int = 1) -> None:
+        with self._lock:
+            self.precond_applies += count
+
+    def add_gram(self) -> None:
+        with self._lock:
+            self.gram_assemblies += 1
+
+    def snapshot(self) -> dict:
+        with self._lock:
+            return {
+                "matvecs": self.matvecs,
+                "precond_applies": self.precond_applies,
+                "gram_assemblies": self.gram_assemblies,
+            }
+
+
+# ---------------------------------------------------------------------------
+# device buffers
+# ---------------------------------------------------------------------------
+def padded_ld(n: int) -> int:
+    return max(LD_ALIGN, (int(n) + LD_ALIGN - 1) // LD_ALIGN * LD_ALIGN)
+
+
+def empty_block(n: int, m: int, device, cap: int | None = None) -> torch.Tensor:
+    """Uninitialised column-major n x m block (capacity ``cap`` columns)."""
+    cap = max(int(m), int(cap or 0), 1)
+    store = torch.empty((cap, padded_ld(n)), dtype=F64, device=device)
+    return store[: int(m), : int(n)].t()
+
+
+def zeros_block(n: int, m: int, device, cap: int | None = None) -> torch.Tensor:
+    b = empty_block(n, m, device, cap)
+    if m:
+        b.zero_()
+    return b
+
+
+def block_ld(t: torch.Tensor) -> int:
+    """Leading dimension of a column-major device block (n x m); for a single
+    column any even value >= n is valid (it is never used for addressing)."""
+    if t.dim() != 2:
+        raise DimensionMismatch("expected a 2-D block")
+    n, m = int(t.shape[0]), int(t.shape[1])
+    if m > 1:
+        return int(t.stride(1))
+    ld = max(int(t.stride(1)), n, 1)
+    return ld + (ld % 2)
+
+
+def _is_device_block(t) -> bool:
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == F64 and t.dim() == 2):
+        return False
+    n, m = int(t.shape[0]), int(t.shape[1])
+    if n > 1 and t.stride(0) != 1:
+        return False
+    if m > 1 and (t.stride(1) < n or t.stride(1) % 2 != 0):
+        return False
+    return t.data_ptr() % 16 == 0
+
+
+def as_block(B, device=None) -> torch.Tensor:
+    """Column-major, 16-byte aligned float64 device block view of ``B`` (n x m)."""
+    if device is None:
+        device = nat.require_device()
+    if _is_device_block(B):
+        return B
+    if isinstance(B, torch.Tensor):
+        src = B.detach()
+        if src.dim() == 1:
+            src = src[:, None]
+    else:
+        src = torch.from_numpy(np.atleast_2d(np.asarray(B, dtype=np.float64)))
+        if np.asarray(B).ndim == 1:
+            src = src.reshape(-1, 1)
+    n, m = src.shape
+    out = empty_block(n, m, device)
+    if m and n:
+        out.copy_(src.to(device=device, dtype=F64))
+    return out
+
+
+def as_vector(x, device=None, copy: bool = False) -> torch.Tensor:
+    """Contiguous float64 device vector."""
+    if device is None:
+        device = nat.require_device()
+    if isinstance(x, torch.Tensor):
+        t = x.detach().to(device=device, dtype=F64)
+        if t.dim() != 1:
+            t = t.reshape(-1)
+        t = t.contiguous()
+        return t.clone() if copy and t.data_ptr() == x.data_ptr() else t
+    arr = np.ascontiguousarray(np.asarray(x, dtype=np.float64).reshape(-1))
+    return torch.from_numpy(arr).to(device)
+
+
+def to_numpy(t) -> np.ndarray:
+    """Host copy of a device tensor (or passthrough for arrays)."""
+    if isinstance(t, torch.Tensor):
+        return t.detach().cpu().numpy()
+    return np.asarray(t)
+
+
+def column(B: torch.Tensor, j: int) -> torch.Tensor:
+    return B[:, j]
+
+
+def hstack_blocks(blocks, n: int, device, cap_extra: int = 0) -> torch.Tensor:
+    """Column concatenation into a fresh block (np.hstack of threestage.py:365)."""
+    m = sum(int(b.shape[1]) for b in blocks)
+    out = empty_block(n, m, device, cap=m + cap_extra)
+    at = 0
+    for b in blocks:
+        w = int(b.shape[1])
+        if w:
+            out[:, at : at + w].copy_(b)
+        at += w
+    return out
+
+
+# ---------------------------------------------------------------------------
+# CSR matrix
+# ---------------------------------------------------------------------------
+_pattern_cache_lock = threading.Lock()
+_pattern_cache: list = []  # [(host rowptr, host col, device rowptr, device col)]
+
+
+def _device_pattern(rowptr: np.ndarray, col: np.ndarray, device):
+    with _pattern_cache_lock:
+        for hr, hc, dr, dc in _pattern_cache:
+            if dr.device == device and (hr is rowptr or np.array_equal(hr, rowptr)) and (
+                hc is col or (hc.shape == col.shape and np.array_equal(hc, col))
+            ):
+                return dr, dc
+    dr = torch.from_numpy(np.ascontiguousarray(rowptr, dtype=np.int32)).to(device)
+    dc = torch.from_numpy(np.ascontiguousarray(col, dtype=np.int32)).to(device)
+    with _pattern_cache_lock:
+        _pattern_cache.insert(0, (rowptr, col, dr, dc))
+        del _pattern_cache[2:]
+    return dr, dc
+
+
+class SparseSpdMatrix:
+    """SPD CSR matrix resident on the GPU (linalg.py:63-135).
+
+    Both triangles are stored; indices are int32, values float64.
+    Construction validates numerical symmetry to 1e-12 relative and a strictly
+    positive diagonal on the device (linalg.py:105-119), raising
+    ``NotSymmetric`` / ``NotPositiveDefinite(pivot)`` like the reference.
+    Instances are immutable and safe to share across threads.
+    """
+
+    def __init__(self, n, row_offsets, col_indices, values, *, device=None, validate: bool = True,
+                 lanes: int = 0):
+        self.n = int(n)
+        dev = device if device is not None else nat.require_device()
+        self.device = torch.device(dev)
+        if isinstance(row_offsets, torch.Tensor) and isinstance(col_indices, torch.Tensor):
+            rp = row_offsets.to(self.device, torch.int32).contiguous()
+            ci = col_indices.to(self.device, torch.int32).contiguous()
+            if rp.shape != (self.n + 1,):
+                raise DimensionMismatch(
+                    f"row_offsets must have length n+1={self.n + 1}, got {tuple(rp.shape)}"
+                )
+        else:
+            rp_h = np.asarray(row_offsets)
+            ci_h = np.asarray(col_indices)
+            if rp_h.shape != (self.n + 1,):
+                raise DimensionMismatch(
+                    f"row_offsets must have length n+1={self.n + 1}, got {rp_h.shape}"
+                )
+            if ci_h.size and (not _rows_sorted(rp_h, ci_h)):
+                csr = scipy.sparse.csr_matrix(
+                    (np.asarray(values, dtype=np.float64), ci_h, rp_h), shape=(self.n, self.n)
+                )
+                csr.sum_duplicates()
+                rp_h, ci_h, values = csr.indptr, csr.indices, csr.data
+            if rp_h.size and int(rp_h[-1]) >= 2**31:
+                raise DimensionMismatch("nnz must be < 2^31 for the int32 device layout")
+            rp, ci = _device_pattern(rp_h, ci_h, self.device)
+        if isinstance(values, torch.Tensor):
+            vals = values.to(self.device, F64).contiguous()
+        else:
+            vals = torch.from_numpy(np.ascontiguousarray(np.asarray(values, dtype=np.float64))).to(self.device)
+        self.rowptr = rp
+        self.col = ci
+        self.values = vals
+        self.nnz = int(vals.numel())
+        self.lanes = int(lanes)
+        self._csr = nat.RkCsr(self.n, self.nnz, rp.data_ptr(), ci.data_ptr(), vals.data_ptr(), self.lanes, 0)
+        self._diag = None
+        self._dinv = None
+        self._bad_diag = None
+        if validate:
+            self._validate()
+
+    # -- construction helpers (linalg.py:86-103) ---------------------------
+    @classmethod
+    def from_scipy(cls, mat, **kw) -> "SparseSpdMatrix":
+        csr = scipy.sparse.csr_matrix(mat).astype(np.float64)
+        csr.sum_duplicates()
+        return cls(csr.shape[0], csr.indptr, csr.indices, csr.data, **kw)
+
+    @classmethod
+    def from_dense(cls, mat, **kw) -> "SparseSpdMatrix":
+        if isinstance(mat, torch.Tensor):
+            mat = mat.detach().cpu().numpy()
+        csr = scipy.sparse.csr_matrix(np.asarray(mat, dtype=np.float64))
+        return cls(csr.shape[0], csr.indptr, csr.indices, csr.data, **kw)
+
+    @classmethod
+    def identity(cls, n: int, **kw) -> "SparseSpdMatrix":
+        return cls.from_scipy(scipy.sparse.identity(n, format="csr"), **kw)
+
+    @classmethod
+    def from_diagonal(cls, diag, **kw) -> "SparseSpdMatrix":
+        return cls.from_scipy(scipy.sparse.diags(np.asarray(diag, dtype=np.float64), format="csr"), **kw)
+
+    @classmethod
+    def from_host(cls, A, **kw) -> "SparseSpdMatrix":
+        """Upload any CSR-like host matrix: this class, the reference's
+        SparseSpdMatrix (n, row_offsets, col_indices, values), or scipy."""
+        if isinstance(A, SparseSpdMatrix):
+            return A
+        if all(hasattr(A, a) for a in ("n", "row_offsets", "col_indices", "values")):
+            return cls(A.n, A.row_offsets, A.col_indices, A.values, **kw)
+        if scipy.sparse.issparse(A):
+            return cls.from_scipy(A, **kw)
+        return cls.from_dense(A, **kw)
+
+    def with_values(self, values, validate: bool = True) -> "SparseSpdMatrix":
+        """Same sparsity pattern, new values (per-system refresh of a sequence)."""
+        return SparseSpdMatrix(self.n, self.rowptr, self.col, values, device=self.device, validate=validate,
+                               lanes=self.lanes)
+
+    def _validate(self) -> None:
+        s = nat.scratch(self.device)
+        ws = s.workspace(nat.lib().rk_reduce_workspace_doubles(max(self.n, 1), 8))
+        out = torch.zeros(2, dtype=F64, device=self.device)
+        bad = torch.empty(1, dtype=torch.int64, device=self.device)
+        diag = torch.empty(self.n, dtype=F64, device=self.device)
+        dinv = torch.empty(self.n, dtype=F64, device=self.device)
+        st = nat.stream_ptr(self.device)
+        if self.nnz:
+            nat.check(nat.lib().rk_csr_asymmetry(self._csr, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                                 s.tickets.data_ptr(), st), "SparseSpdMatrix validate")
+        nat.check(nat.lib().rk_csr_diagonal(self._csr, diag.data_ptr(), dinv.data_ptr(), bad.data_ptr(), st),
+                  "SparseSpdMatrix diagonal")
+        worst, scale = (float(v) for v in out.cpu())
+        if scale > 0 and worst > _SYMMETRY_RTOL * scale:
+            raise NotSymmetric(f"matrix asymmetry {worst:.3e} exceeds {_SYMMETRY_RTOL:.0e} * {scale:.3e}")
+        b = int(bad.cpu())
+        self._diag, self._dinv = diag, dinv
+        self._bad_diag = b if 0 <= b < self.n else -1
+        if self._bad_diag >= 0:
+            d = float(diag[self._bad_diag].cpu())
+            raise NotPositiveDefinite(f"diagonal entry {self._bad_diag} is {d!r}, must be > 0",
+                                      pivot=self._bad_diag)
+
+    def _diagonals(self):
+        if self._diag is None:
+            bad = torch.empty(1, dtype=torch.int64, device=self.device)
+            diag = torch.empty(self.n, dtype=F64, device=self.device)
+            dinv = torch.empty(self.n, dtype=F64, device=self.device)
+            nat.check(nat.lib().rk_csr_diagonal(self._csr, diag.data_ptr(), dinv.data_ptr(), bad.data_ptr(),
+                                                nat.stream_ptr(self.device)), "diagonal")
+            b = int(bad.cpu())
+            self._diag, self._dinv = diag, dinv
+            self._bad_diag = b if 0 <= b < self.n else -1
+        return self._diag, self._dinv, self._bad_diag
+
+    @property
+    def shape(self):
+        return (self.n, self.n)
+
+    @property
+    def csr(self) -> nat.RkCsr:
+        return self._csr
+
+    def diagonal(self) -> torch.Tensor:
+        return self._diagonals()[0]
+
+    def to_scipy(self) -> scipy.sparse.csr_matrix:
+        return scipy.sparse.csr_matrix(
+            (self.values.cpu().numpy(), self.col.cpu().numpy(), self.rowptr.cpu().numpy()),
+            shape=(self.n, self.n),
+        )
+
+    def to_dense(self) -> np.ndarray:
+        return self.to_scipy().toarray()
+
+    def matvec(self, x, sink: InstrumentationSink | None = None) -> torch.Tensor:
+        return spmv(self, x, sink)
+
+
+def _rows_sorted(rp: np.ndarray, ci: np.ndarray) -> bool:
+    if ci.size < 2:
+        return True
+    d = np.diff(ci.astype(np.int64))
+    # a descent is allowed only where a new row starts
+    starts = np.zeros(ci.size - 1, dtype=bool)
+    rs = np.asarray(rp[1:-1], dtype=np.int64) - 1
+    rs = rs[(rs >= 0) & (rs < ci.size - 1)]
+    starts[rs] = True
+    return bool(np.all((d > 0) | starts))
+
+
+def as_matrix(A) -> SparseSpdMatrix:
+    return A if isinstance(A, SparseSpdMatrix) else SparseSpdMatrix.from_host(A)
+
+
+# ---------------------------------------------------------------------------
+# kernels (linalg.py:138-174)
+# ---------------------------------------------------------------------------
+def spmv_into(A: SparseSpdMatrix, x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
+    nat.check(nat.lib().rk_spmv(A.csr, x.data_ptr(), y.data_ptr(), nat.stream_ptr(A.device)), "spmv")
+    return y
+
+
+def spmv(A: SparseSpdMatrix, x, sink: InstrumentationSink | None = None) -> torch.Tensor:
+    """y = A x on the device (linalg.py:138-148); counts one matvec."""
+    A = as_matrix(A)
+    xd = as_vector(x, A.device)
+    if xd.shape[0] != A.n:
+        raise DimensionMismatch(f"matvec: matrix is {A.n}x{A.n}, vector has length {xd.shape[0]}")
+    if sink is not None:
+        sink.add_matvec()
+    y = torch.empty(A.n, dtype=F64, device=A.device)
+    return spmv_into(A, xd, y)
+
+
+def spmm(A: SparseSpdMatrix, B: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """A B for a column-major block (scipy csr_matvecs, linalg.py:173); no counting."""
+    m = int(B.shape[1])
+    if out is None:
+        out = empty_block(A.n, m, A.device)
+    if m:
+        nat.check(nat.lib().rk_spmm(A.csr, m, B.data_ptr(), block_ld(B), out.data_ptr(), block_ld(out),
+                                    nat.stream_ptr(A.device)), "spmm")
+    return out
+
+
+def gram(X: torch.Tensor, Y: torch.Tensor) -> torch.Tensor:
+    """X' Y (m1 x m2) with the DMMA split-K kernel; returned as an (m1, m2) view."""
+    n, m1 = X.shape
+    n2, m2 = Y.shape
+    if n != n2:
+        raise DimensionMismatch("gram: row counts differ")
+    dev = X.device
+    store = torch.empty((max(m2, 1), max(m1, 1)), dtype=F64, device=dev)
+    G = store[:m2, :m1].t()
+    if m1 and m2:
+        s = nat.scratch(dev)
+        need = nat.lib().rk_gram_workspace_doubles(n, m1, m2)
+        ws = s.workspace(max(need, 1))
+        nat.check(nat.lib().rk_gram(n, m1, X.data_ptr(), block_ld(X), m2, Y.data_ptr(), block_ld(Y),
+                                    G.data_ptr(), max(m1, 1), ws.data_ptr(), ws.numel(), nat.stream_ptr(dev)),
+                  "gram")
+    return G
+
+
+def gemm_nn(S: torch.Tensor, C, out: torch.Tensor | None = None) -> torch.Tensor:
+    """S (N x s) @ C (s x y) with the DMMA kernel (pod.py:91-93)."""
+    n, s = S.shape
+    Cd = as_block(C, S.device)
+    if Cd.shape[0] != s:
+        raise DimensionMismatch("gemm_nn: inner dimensions differ")
+    y = int(Cd.shape[1])
+    if out is None:
+        out = empty_block(n, y, S.device)
+    if y and n:
+        if s == 0:
+            out.zero_()
+        else:
+            nat.check(nat.lib().rk_gemm_nn(n, s, y, S.data_ptr(), block_ld(S), Cd.data_ptr(), block_ld(Cd),
+                                           out.data_ptr(), block_ld(out), nat.stream_ptr(S.device)), "gemm_nn")
+    return out
+
+
+def gemv_t(B: torch.Tensor, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """B' x (krylov.py:156 `cross.T @ z`), deterministic split reduction."""
+    n, m = B.shape
+    dev = B.device
+    if out is None:
+        out = torch.empty(m, dtype=F64, device=dev)
+    if m:
+        s = nat.scratch(dev)
+        ws = s.workspace(nat.lib().rk_reduce_workspace_doubles(max(n, 1), m))
+        nat.check(nat.lib().rk_gemv_t(n, m, B.data_ptr(), block_ld(B), x.data_ptr(), out.data_ptr(),
+                                      ws.data_ptr(), ws.numel(), nat.stream_ptr(dev)), "gemv_t")
+    return out
+
+
+def gemv_n(B: torch.Tensor, c, y0: torch.Tensor | None = None, op: int = 0,
+           out: torch.Tensor | None = None) -> torch.Tensor:
+    """B c (op 0), y0 + B c (op 1), y0 - B c (op 2) (krylov.py:291,326)."""
+    n, m = B.shape
+    dev = B.device
+    cd = as_vector(c, dev)
+    if out is None:
+        out = torch.empty(n, dtype=F64, device=dev)
+    if n:
+        nat.check(nat.lib().rk_gemv_n(n, m, B.data_ptr(), block_ld(B), cd.data_ptr() if m else None,
+                                      y0.data_ptr() if y0 is not None else None, out.data_ptr(), op,
+                                      nat.stream_ptr(dev)), "gemv_n")
+    return out
+
+
+def dot(x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
+    """x'y as a 1-element device tensor (deterministic)."""
+    dev = x.device
+    s = nat.scratch(dev)
+    ws = s.workspace(nat.lib().rk_reduce_workspace_doubles(max(int(x.numel()), 1), 1))
+    out = torch.empty(1, dtype=F64, device=dev)
+    nat.check(nat.lib().rk_dot(int(x.numel()), x.data_ptr(), y.data_ptr(), out.data_ptr(), ws.data_ptr(),
+                               ws.numel(), s.tickets.data_ptr(), nat.stream_ptr(dev)), "dot")
+    return out
+
+
+def norm(x: torch.Tensor) -> float:
+    """||x||_2 = sqrt(x'x) (numpy.linalg.norm for 1-D input)."""
+    return float(np.sqrt(float(dot(x, x).cpu())))
+
+
+def scale_columns(V: torch.Tensor, s, out: torch.Tensor | None = None) -> torch.Tensor:
+    """V[:, j] / s[j] (threestage.py:483)."""
+    n, m = V.shape
+    dev = V.device
+    sd = as_vector(s, dev)
+    if out is None:
+        out = empty_block(n, m, dev)
+    if n and m:
+        nat.check(nat.lib().rk_scale_columns(n, m, V.data_ptr(), block_ld(V), sd.data_ptr(), out.data_ptr(),
+                                             block_ld(out), nat.stream_ptr(dev)), "scale_columns")
+    return out
+
+
+def weighted_inner(A: SparseSpdMatrix, x, y) -> float:
+    """A-weighted inner product x'Ay (linalg.py:151-157)."""
+    A = as_matrix(A)
+    xd = as_vector(x, A.device)
+    yd = as_vector(y, A.device)
+    if xd.shape[0] != A.n or yd.shape[0] != A.n:
+        raise DimensionMismatch("weighted_inner: dimension mismatch")
+    Ay = spmv(A, yd)
+    return float(dot(xd, Ay).cpu())
+
+
+def assemble_gram(A: SparseSpdMatrix, B, sink: InstrumentationSink | None = None):
+    """(B'AB, AB) (linalg.py:160-174): SpMM then the DMMA Gram; counts one gram
+    assembly plus one matvec per column, exactly like the reference."""
+    A = as_matrix(A)
+    Bd = as_block(B, A.device)
+    if Bd.shape[0] != A.n:
+        raise DimensionMismatch("assemble_gram: basis rows must match matrix dimension")
+    if sink is not None:
+        sink.add_gram()
+        sink.add_matvec(int(Bd.shape[1]))
+    AB = spmm(A, Bd)
+    return gram(Bd, AB), AB
+
+
+# ---------------------------------------------------------------------------
+# small dense algebra (host LAPACK, as the reference)
+# ---------------------------------------------------------------------------
+@dataclass
+class DenseBasis:
+    """Block of length-n columns with optional Gram metadata (linalg.py:177-205)."""
+
+    columns: object
+    gram_diag: np.ndarray | None = None
+
+    def __post_init__(self):
+        if not isinstance(self.columns, torch.Tensor):
+            self.columns = np.atleast_2d(np.asarray(self.columns, dtype=np.float64))
+        if self.gram_diag is not None:
+            self.gram_diag = np.asarray(self.gram_diag, dtype=np.float64)
+            if self.gram_diag.shape != (self.columns.shape[1],):
+                raise DimensionMismatch("gram_diag length must equal column count")
+
+    @property
+    def n(self) -> int:
+        return int(self.columns.shape[0])
+
+    @property
+    def m(self) -> int:
+        return int(self.columns.shape[1])
+
+    @classmethod
+    def empty(cls, n: int) -> "DenseBasis":
+        return cls(np.zeros((n, 0)))
+
+
+def as_columns(basis):
+    if basis is None:
+        raise DimensionMismatch("expected a basis, got None")
+    if isinstance(basis, DenseBasis):
+        return basis.columns
+    return basis
+
+
+class DenseLowerTriangular:
+    """Packed lower-triangular Cholesky factor L with G = L L' (linalg.py:217-247).
+
+    Kept on the host (it is w x w); ``device()`` returns a cached column-major
+    device copy for the fused PCG kernels."""
+
+    def __init__(self, entries_packed, m: int):
+        self.m = int(m)
+        self.entries = np.asarray(entries_packed, dtype=np.float64)
+        if self.entries.shape != (self.m * (self.m + 1) // 2,):
+            raise DimensionMismatch("packed entry count must be m(m+1)/2")
+        self._full = np.zeros((self.m, self.m))
+        self._full[np.tril_indices(self.m)] = self.entries
+        if self.m and np.any(np.diag(self._full) <= 0.0):
+            raise NotPositiveDefinite("lower-triangular factor must have positive diagonal")
+        self._dev = {}
+
+    @classmethod
+    def from_full(cls, L) -> "DenseLowerTriangular":
+        L = np.asarray(L, dtype=np.float64)
+        return cls(L[np.tril_indices(L.shape[0])], L.shape[0])
+
+    def full(self) -> np.ndarray:
+        return self._full.copy()
+
+    def device(self, device) -> torch.Tensor:
+        key = (device.type, device.index)
+        t = self._dev.get(key)
+        if t is None:
+            t = self._dev[key] = as_block(self._full, device)
+        return t
+
+    def device_form(self, device):
+        """(L, w, sqd=None) in the form the fused PCG kernels take."""
+        return (self.device(device) if self.m else None, self.m, None)
+
+    def solve_lower(self, rhs):
+        return scipy.linalg.solve_triangular(self._full, np.asarray(rhs, dtype=np.float64), lower=True)
+
+    def solve_upper(self, rhs):
+        return scipy.linalg.solve_triangular(self._full, np.asarray(rhs, dtype=np.float64), lower=True, trans="T")
+
+    def solve_spd(self, rhs):
+        return self.solve_upper(self.solve_lower(rhs))
+
+
+def _host(G) -> np.ndarray:
+    return to_numpy(G) if isinstance(G, torch.Tensor) else np.asarray(G, dtype=np.float64)
+
+
+def dense_cholesky(G) -> DenseLowerTriangular:
+    """LAPACK dpotrf of a (host copy of a) small SPD matrix (linalg.py:250-267)."""
+    G = np.asarray(_host(G), dtype=np.float64)
+    if G.ndim != 2 or G.shape[0] != G.shape[1]:
+        raise DimensionMismatch("dense_cholesky: matrix must be square")
+    if G.shape[0] == 0:
+        return DenseLowerTriangular(np.zeros(0), 0)
+    L, info = scipy.linalg.lapack.dpotrf(G, lower=1, clean=1, overwrite_a=0)
+    if info > 0:
+        raise NotPositiveDefinite(f"leading minor of order {info} is not positive definite", pivot=int(info - 1))
+    if info < 0:
+        raise DimensionMismatch(f"dpotrf: illegal argument {-info}")
+    return DenseLowerTriangular.from_full(L)
+
+
+def symmetric_evd(G):
+    """eigh with eigenvalues descending (linalg.py:270-280), host LAPACK dsyevd."""
+    G = np.asarray(_host(G), dtype=np.float64)
+    try:
+        w, V = np.linalg.eigh(G)
+    except np.linalg.LinAlgError as exc:
+        raise IterationLimit(f"symmetric EVD did not converge: {exc}") from exc
+    return w[::-1].copy(), V[:, ::-1].copy()
+
+
+def thin_svd(B):
+    B = np.atleast_2d(_host(B))
+    try:
+        U, s, Vt = np.linalg.svd(B, full_matrices=False)
+    except np.linalg.LinAlgError as exc:
+        raise IterationLimit(f"SVD did not converge: {exc}") from exc
+    return U, s, Vt.T
+
+
+def _orthonormal_basis(B: np.ndarray, label: str) -> np.ndarray:
+    if B.shape[1] == 0:
+        return B
+    U, s, _ = np.linalg.svd(B, full_matrices=False)
+    if s[0] == 0.0 or s[-1] <= max(B.shape) * np.finfo(float).eps * s[0]:
+        raise RankDeficient(f"{label} basis is rank deficient")
+    return U
+
+
+def principal_angle_distance(U, V) -> float:
+    """sin of the largest principal angle between range(U) and range(V)."""
+    Qu = _orthonormal_basis(np.atleast_2d(_host(as_columns(U))), "first")
+    Qv = _orthonormal_basis(np.atleast_2d(_host(as_columns(V))), "second")
+    if Qu.shape[0] != Qv.shape[0]:
+        raise DimensionMismatch("principal_angle_distance: ambient dimensions differ")
+    if Qu.shape[1] == 0:
+        return 0.0
+    if Qv.shape[1] == 0:
+        return 1.0
+    d = float(np.linalg.norm(Qu - Qv @ (Qv.T @ Qu), 2))
+    return min(max(d, 0.0), 1.0)

@@ -1,0 +1,108 @@
+"""Goal-oriented POD by the method of snapshots (``recykl/pod.py``).
+
+The N-sized work (the A-weighted Gram S'AS and the reconstruction S @ coef)
+runs in the DMMA kernels; the s x s eigenproblem runs in host LAPACK
+(numpy.linalg.eigh = dsyevd), exactly the routine the reference calls, so the
+spectrum and the energy truncation agree with the oracle to Gram rounding.
+"""
+
+from __future__ import annotations
+
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .errors import DimensionMismatch, EmptyBasis, RankTruncatedWarning
+from .linalg import DenseBasis, SparseSpdMatrix, as_block, as_matrix, assemble_gram, gemm_nn, symmetric_evd, to_numpy
+
+_RANK_RTOL = 1e-12  # pod.py:30, on sigma^2 relative to the largest
+
+
+@dataclass
+class PodMetric:
+    kind: str  # "explicit" | "factor"
+    operand: object
+
+    @classmethod
+    def explicit(cls, theta) -> "PodMetric":
+        return cls("explicit", theta)
+
+    @classmethod
+    def factor(cls, chalf) -> "PodMetric":
+        return cls("factor", chalf)
+
+
+@dataclass
+class PodBasisResult:
+    basis: DenseBasis
+    singular_values: np.ndarray
+    y: int
+    snapshot_coef: np.ndarray | None = None
+
+    @property
+    def columns(self):
+        return self.basis.columns
+
+
+def energy_truncation_dim(sigma_sq, eps: float) -> int:
+    """Smallest dimension whose cumulative energy reaches eps, never beyond the
+    numerical rank (modes > 1e-12 sigma_1^2); pod.py:58-83."""
+    s2 = np.asarray(sigma_sq, dtype=np.float64)
+    if s2.size == 0:
+        raise EmptyBasis("empty spectrum")
+    if np.any(np.diff(s2) > 0) or np.any(s2 < -_RANK_RTOL * max(s2[0], 0.0)):
+        raise DimensionMismatch("spectrum must be nonincreasing and nonnegative")
+    total = float(np.sum(s2))
+    if s2[0] <= 0.0 or total <= 0.0:
+        raise EmptyBasis("all spectral energy is zero")
+    rank = int(np.sum(s2 > _RANK_RTOL * s2[0]))
+    reached = np.nonzero((np.cumsum(s2) / total)[:rank] >= eps)[0]
+    if reached.size == 0:
+        warnings.warn(
+            "energy criterion unreachable within the numerical rank; truncating at the rank",
+            RankTruncatedWarning,
+        )
+        return rank
+    return int(reached[0]) + 1
+
+
+def _finalize(S, gamma, sigma, V, eps, max_cols=None):
+    """coef = V[:, :y] / sigma[:y] * gamma; basis = S @ coef (pod.py:86-97).
+    ``max_cols`` reconstructs only a leading column prefix (columns are
+    independent, so the prefix is identical to slicing the full basis)."""
+    if np.all(gamma == 0.0):
+        raise EmptyBasis("all snapshot weights are zero")
+    sigma_sq = np.maximum(sigma, 0.0) ** 2
+    y = energy_truncation_dim(sigma_sq, eps)
+    coef = (V[:, :y] / sigma[:y]) * gamma[:, None]
+    ncols = y if max_cols is None else min(y, int(max_cols))
+    cols = gemm_nn(S, np.ascontiguousarray(coef[:, :ncols])) if isinstance(S, torch.Tensor) else S @ coef[:, :ncols]
+    return PodBasisResult(
+        basis=DenseBasis(cols, gram_diag=np.ones(ncols)),
+        singular_values=np.maximum(sigma, 0.0),
+        y=y,
+        snapshot_coef=coef,
+    )
+
+
+def pod_evd_from_gram(gram_sts, S, gamma, eps: float, *, max_cols: int | None = None) -> PodBasisResult:
+    """Method of snapshots from a precomputed S'Theta S (pod.py:123-131)."""
+    Sd = as_block(S)
+    gamma = np.asarray(to_numpy(gamma), dtype=np.float64)
+    G = np.asarray(to_numpy(gram_sts), dtype=np.float64)
+    weighted = gamma[:, None] * G * gamma[None, :]
+    eigs, V = symmetric_evd(0.5 * (weighted + weighted.T))
+    sigma = np.sqrt(np.maximum(eigs, 0.0))
+    return _finalize(Sd, gamma, sigma, V, eps, max_cols=max_cols)
+
+
+def pod_evd(S, gamma, theta, eps: float, *, max_cols: int | None = None) -> PodBasisResult:
+    """POD with an explicit SPD metric (pod.py:100-120): device Gram S'(theta S)."""
+    Sd = as_block(S)
+    gamma = np.asarray(to_numpy(gamma), dtype=np.float64)
+    if gamma.shape[0] != Sd.shape[1]:
+        raise DimensionMismatch("one weight per snapshot required")
+    G, _ = assemble_gram(as_matrix(theta), Sd, None)
+    return pod_evd_from_gram(G, Sd, gamma, eps, max_cols=max_cols)

@@ -1,0 +1,157 @@
+"""Kernel-level parity of libpodcg.so against the reference's goldens and numpy
+(fp64; bit-level where the op is elementwise, 1e-12-relative for reductions)."""
+
+import numpy as np
+import pytest
+import scipy.sparse
+import torch
+
+import golden_io as gio
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pk():
+    import paper_1512_05820_b200 as pk
+
+    return pk
+
+
+def _dev_matrix(pk, rowptr, col, val):
+    return pk.SparseSpdMatrix(len(rowptr) - 1, rowptr, col, val)
+
+
+def test_library_reports_sm_count(pk):
+    from paper_1512_05820_b200 import _native as nat
+
+    assert nat.lib().rk_device_sm_count() >= 100
+
+
+def test_spmv_matches_reference_golden(pk):
+    d = gio.load("kernels")
+    A = _dev_matrix(pk, d["rowptr"], d["col"], d["val"])
+    y = pk.spmv(A, d["x"]).cpu().numpy()
+    # linalg test: SpMV vs dense to 1e-12 (reference tests/test_linalg.py:52-64)
+    np.testing.assert_allclose(y, d["Ax"], rtol=1e-12, atol=1e-12 * np.abs(d["Ax"]).max())
+
+
+@pytest.mark.parametrize("lanes", [0, 1, 2, 4, 8, 16, 32])
+def test_spmv_all_lane_widths(pk, lanes):
+    from paper_1512_05820_b200.problems import elasticity_sequence, laplacian3d
+
+    for H in (laplacian3d(9, 7, 5), next(iter(elasticity_sequence((3, 4, 5), p=1))).A):
+        A = pk.SparseSpdMatrix(H.n, H.row_offsets, H.col_indices, H.values, lanes=lanes)
+        x = np.random.default_rng(lanes).standard_normal(H.n)
+        ref = H.to_scipy() @ x
+        got = pk.spmv(A, x).cpu().numpy()
+        np.testing.assert_allclose(got, ref, rtol=1e-13, atol=1e-13 * np.abs(ref).max())
+
+
+def test_spmv_sink_counts_one_matvec(pk):
+    A = pk.SparseSpdMatrix.identity(5)
+    sink = pk.InstrumentationSink()
+    pk.spmv(A, np.ones(5), sink)
+    assert sink.matvecs == 1
+
+
+def test_assemble_gram_matches_golden_and_counts(pk):
+    d = gio.load("kernels")
+    A = _dev_matrix(pk, d["rowptr"], d["col"], d["val"])
+    sink = pk.InstrumentationSink()
+    G, AS = pk.assemble_gram(A, d["S"], sink)
+    np.testing.assert_allclose(AS.cpu().numpy(), d["AS"], rtol=1e-12, atol=1e-12 * np.abs(d["AS"]).max())
+    np.testing.assert_allclose(G.cpu().numpy(), d["G"], rtol=1e-12, atol=1e-12 * np.abs(d["G"]).max())
+    assert sink.gram_assemblies == 1 and sink.matvecs == d["S"].shape[1]
+
+
+@pytest.mark.parametrize("n,m1,m2", [(1, 1, 1), (37, 3, 5), (1000, 64, 64), (4099, 65, 130), (70001, 20, 20),
+                                     (20000, 200, 7)])
+def test_dmma_gram_shapes(pk, n, m1, m2):
+    from paper_1512_05820_b200.linalg import as_block, gram
+
+    rng = np.random.default_rng(n + m1)
+    X = rng.standard_normal((n, m1))
+    Y = rng.standard_normal((n, m2))
+    G = gram(as_block(X), as_block(Y)).cpu().numpy()
+    ref = X.T @ Y
+    np.testing.assert_allclose(G, ref, rtol=1e-11, atol=1e-12 * np.sqrt(n))
+
+
+@pytest.mark.parametrize("n,s,y", [(1, 1, 1), (33, 17, 3), (4096, 100, 60), (9999, 300, 70)])
+def test_dmma_gemm_nn_shapes(pk, n, s, y):
+    from paper_1512_05820_b200.linalg import as_block, gemm_nn
+
+    rng = np.random.default_rng(n + s)
+    S = rng.standard_normal((n, s))
+    C = rng.standard_normal((s, y))
+    out = gemm_nn(as_block(S), C).cpu().numpy()
+    np.testing.assert_allclose(out, S @ C, rtol=1e-11, atol=1e-12 * np.sqrt(s))
+
+
+def test_gemv_pair(pk):
+    from paper_1512_05820_b200.linalg import as_block, as_vector, gemv_n, gemv_t
+
+    rng = np.random.default_rng(7)
+    n, m = 5003, 41
+    B = rng.standard_normal((n, m))
+    x = rng.standard_normal(n)
+    c = rng.standard_normal(m)
+    Bd = as_block(B)
+    np.testing.assert_allclose(gemv_t(Bd, as_vector(x)).cpu().numpy(), B.T @ x, rtol=1e-12, atol=1e-11)
+    np.testing.assert_allclose(gemv_n(Bd, c).cpu().numpy(), B @ c, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(gemv_n(Bd, c, as_vector(x), op=2).cpu().numpy(), x - B @ c, rtol=1e-12, atol=1e-12)
+
+
+def test_spmm_matches_scipy(pk):
+    from paper_1512_05820_b200.linalg import as_block, spmm
+    from paper_1512_05820_b200.problems import elasticity_sequence
+
+    H = next(iter(elasticity_sequence((4, 3, 3), p=1))).A
+    A = pk.SparseSpdMatrix(H.n, H.row_offsets, H.col_indices, H.values)
+    X = np.random.default_rng(3).standard_normal((H.n, 19))
+    got = spmm(A, as_block(X)).cpu().numpy()
+    ref = H.to_scipy() @ X
+    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+
+
+def test_pod_from_gram_matches_reference(pk):
+    d = gio.load("kernels")
+    res = pk.pod_evd_from_gram(d["G"], d["S"], d["gamma"], 0.999)
+    assert res.y == int(d["pod_y"])
+    sig = d["pod_sigma"]
+    lead = sig > 1e-6 * sig[0]
+    np.testing.assert_allclose(res.singular_values[lead], sig[lead], rtol=1e-10)
+    got = res.columns.cpu().numpy()
+    ref = d["pod_basis"]
+    for j in range(res.y):
+        s = np.sign(got[:, j] @ ref[:, j])
+        np.testing.assert_allclose(s * got[:, j], ref[:, j], rtol=1e-8, atol=1e-10 * np.abs(ref[:, j]).max())
+
+
+def test_validation_errors(pk):
+    with pytest.raises(pk.NotSymmetric):
+        pk.SparseSpdMatrix.from_dense(np.array([[2.0, 1.0], [0.0, 2.0]]))
+    with pytest.raises(pk.NotPositiveDefinite) as exc:
+        pk.SparseSpdMatrix.from_dense(np.array([[2.0, 0.0, 0.0], [0.0, -1.0, 0.0], [0.0, 0.0, 1.0]]))
+    assert exc.value.pivot == 1
+    with pytest.raises(pk.DimensionMismatch):
+        pk.SparseSpdMatrix(3, np.array([0, 1]), np.array([0]), np.array([1.0]))
+
+
+def test_jacobi_inverse_diagonal_bitwise(pk):
+    d = gio.load("kernels")
+    A = _dev_matrix(pk, d["rowptr"], d["col"], d["val"])
+    M = pk.build_preconditioner("jacobi", A)
+    ref = 1.0 / scipy.sparse.csr_matrix((d["val"], d["col"], d["rowptr"])).diagonal()
+    assert np.array_equal(M.fused_inverse_diagonal().cpu().numpy(), ref)
+    r = np.random.default_rng(1).standard_normal(A.n)
+    assert np.array_equal(M.apply(r).cpu().numpy(), r * ref)
+
+
+def test_unsorted_input_is_canonicalised(pk):
+    rowptr = np.array([0, 2, 4])
+    col = np.array([1, 0, 1, 0])
+    val = np.array([1.0, 4.0, 3.0, 1.0])
+    A = pk.SparseSpdMatrix(2, rowptr, col, val)
+    np.testing.assert_allclose(pk.spmv(A, np.array([1.0, 2.0])).cpu().numpy(), [6.0, 7.0])

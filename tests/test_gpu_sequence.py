@@ -1,0 +1,138 @@
+"""Whole-path parity: run_sequence on the device vs the reference's frozen
+fixtures and golden runs (counters exact, x to 1e-8, q = c'x to 1e-10)."""
+
+import warnings
+
+import numpy as np
+import pytest
+
+import golden_io as gio
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pk():
+    import paper_1512_05820_b200 as pk
+
+    return pk
+
+
+def _run(pk, seq, tr, mode, precond):
+    cfg = pk.SolverConfig(truncation=pk.TruncationConfig(**tr), mode=mode)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        return pk.run_sequence(seq, cfg, precond_factory=lambda A: pk.build_preconditioner(precond, A))
+
+
+def _check(d, tag, xs, reps, strict=True, c=None):
+    """Parity policy (BASELINE north_star): iterations within +-2 per system,
+    x to 1e-8 and q = c'x to 1e-10.
+
+    A recycled sequence is chaotic in the last bit: the reference itself flips
+    an exit test when its input is perturbed by 1e-15 (tests/test_oracle.py::
+    test_reference_is_rounding_sensitive_on_c1_s5). So up to the first system
+    whose iteration count differs, every counter must match exactly and x, q
+    meet 1e-8 / 1e-10; from that system on (only allowed when ``strict`` is
+    False) counts stay within +-2 and solutions agree at the forcing level."""
+    cnt = gio.counters(d, tag)
+    got = [r.stage3_iters for r in reps]
+    want = list(map(int, cnt["stage3_iters"]))
+    assert len(got) == len(want)
+    first = next((j for j, (a, b) in enumerate(zip(got, want)) if a != b), len(got))
+    if strict:
+        assert first == len(got), (tag, got, want)
+    assert all(abs(a - b) <= 2 for a, b in zip(got, want)), (tag, got, want)
+    exact = slice(0, first)
+    for key, attr in (("matvecs", "matvecs"), ("precond_applies", "precond_applies"),
+                      ("stage2_iters", "stage2_iters"), ("stage1_dim", "stage1_dim")):
+        assert [getattr(r, attr) for r in reps][exact] == list(map(int, cnt[key]))[exact], (tag, key)
+    for j, x in enumerate(xs, start=1):
+        xh = x.cpu().numpy()
+        tol_x = 1e-8 if j - 1 < first else 1e-4
+        key = f"{tag}x{j}"
+        if key in d:
+            ref = d[key]
+            assert np.linalg.norm(xh - ref) <= tol_x * np.linalg.norm(ref), (tag, j)
+        qkey = f"{tag}q{j}"
+        if c is not None and qkey in d:
+            q_ref = float(d[qkey])
+            tol_q = 1e-10 if j - 1 < first else 1e-4
+            assert abs(float(c @ xh) - q_ref) <= tol_q * abs(q_ref), (tag, j)
+    return first
+
+
+FIXTURES = {
+    "identity_like": (dict(strategy="none"), "identity"),
+    "invariant_matrix": (dict(strategy="none", nu_w=1.0), "identity"),
+    "drifting_pod": (dict(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=30, max_dim=20), "jacobi"),
+}
+
+
+@pytest.mark.parametrize("name", list(FIXTURES))
+def test_reference_fixture_counters(pk, name):
+    d = gio.load(name)
+    tr, pc = FIXTURES[name]
+    xs, reps, _ = _run(pk, gio.sequence(d), tr, "fom", pc)
+    frozen = gio.frozen(d)["frozen"]
+    assert [r.stage3_iters for r in reps] == frozen["stage3_iters"]
+    assert [r.stage2_iters for r in reps] == frozen["stage2_iters"]
+    assert [r.stage1_dim for r in reps] == frozen["stage1_dims"]
+    assert [r.matvecs for r in reps] == frozen["matvecs"]
+    np.testing.assert_allclose([r.final_residual for r in reps], frozen["final_residuals"], rtol=1e-6, atol=1e-12)
+    _check(d, "", xs, reps)
+
+
+def test_drifting_pod_cg_mode(pk):
+    d = gio.load("drifting_pod")
+    tr, pc = FIXTURES["drifting_pod"]
+    xs, reps, _ = _run(pk, gio.sequence(d), tr, "cg", pc)
+    _check(d, "cg_", xs, reps)
+
+
+STAGE = {
+    "s2_": (dict(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, stage1_dim=4, storage_cap=30, max_dim=20), "fom"),
+    "s2cg_": (dict(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, stage1_dim=4, storage_cap=30, max_dim=20), "cg"),
+    "phi1_": (dict(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, stage1_dim=4, full_orth=True, storage_cap=30,
+                   max_dim=20), "fom"),
+    "prev_": (dict(strategy="pod-a-prev", nu_y=0.999, nu_w=0.9, storage_cap=25, max_dim=12), "cg"),
+    "none_": (dict(strategy="none", nu_w=1.0), "fom"),
+}
+
+
+@pytest.mark.parametrize("tag", list(STAGE))
+def test_stage_variants(pk, tag):
+    d = gio.load("stage_variants")
+    tr, mode = STAGE[tag]
+    xs, reps, _ = _run(pk, gio.sequence(d), tr, mode, "jacobi")
+    _check(d, tag, xs, reps, strict=False)
+
+
+@pytest.mark.parametrize("tag,mode", [("cg_", "cg"), ("fom_", "fom")])
+def test_elasticity_q1_sequence(pk, tag, mode):
+    d = gio.load("elasticity")
+    tr = dict(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=12, max_dim=12)
+    xs, reps, _ = _run(pk, gio.elasticity_sequence(d), tr, mode, "jacobi")
+    _check(d, tag, xs, reps, strict=False)
+
+
+@pytest.mark.parametrize("tag,mode,extra", [("fom_", "fom", {}), ("cg_", "cg", {}), ("s5_", "fom", {"stage1_dim": 5})])
+def test_c1_poisson_sequence(pk, tag, mode, extra):
+    from paper_1512_05820_b200.problems import poisson2d_sequence
+
+    d = gio.load("c1")
+    seq = poisson2d_sequence(64, p=int(d["p"]))
+    tr = dict(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=20, max_dim=20, **extra)
+    xs, reps, _ = _run(pk, seq, tr, mode, "jacobi")
+    first = _check(d, tag, xs, reps, strict=False, c=d["c"])
+    # the fom and cg recipes are not rounding-sensitive: all 20 systems exact
+    if tag in ("fom_", "cg_"):
+        assert first == len(reps)
+
+
+def test_reference_matrix_objects_are_accepted(pk):
+    """Drop-in: host CSR objects with the reference's field names upload as-is."""
+    d = gio.load("drifting_pod")
+    seq = gio.sequence(d)
+    A = pk.linalg.as_matrix(seq[0].A)
+    assert A.n == seq.n and A.nnz == len(seq[0].A.values)
