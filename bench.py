@@ -1,0 +1,454 @@
+"""Benchmark of the B200 POD-augmented CG hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--systems P] [--mode cg|fom]
+
+Workload (BASELINE configs[2], the north-star sequence): Q1
+hexahedral linear elasticity on 64^3 elements (N = 811,200, nnz =
+63,695,790), 40 systems with drifting moduli and a rotating traction, Jacobi,
+rtol 1e-5, POD basis <= 60 (pod-a-rbf, storage_cap = max_dim = 60,
+nu_w = 1), CG recurrence. Seeded synthetic inputs with those shapes stand in
+for the paper's unavailable Sierra matrices.
+
+One step = one full sequence solve (all P systems through run_sequence).
+``value`` is the device-resident sequence time (all matrices and right-hand
+sides already in HBM); ``e2e`` is the same through the public API from host
+CSR arrays (values + rhs H2D and every solution D2H inside the timed region).
+Inputs (780 MB of CSR per SpMV) exceed L2, so no flush is needed.
+
+``--impl reference`` times the CPU oracle port (the reference is pure Python,
+so there is nothing to compile into oracle/_ref) on a bounded sample and
+scales it to the same metric with the iteration schedule of the GPU run.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+import warnings
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+warnings.simplefilter("ignore")
+
+METRIC = "sequence solve time"
+UNIT = "s"
+SCHEDULE = os.path.join(ROOT, "profiles", "c3_schedule.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--systems", type=int, default=40)
+    ap.add_argument("--mode", default="cg", choices=["cg", "fom"])
+    ap.add_argument("--grid", type=int, default=64)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def workload_config(args, n=None, nnz=None):
+    return {
+        "workload": f"C3 Q1 elasticity {args.grid}^3 elements, {args.systems}-system recycled sequence",
+        "systems": args.systems,
+        "n": n,
+        "nnz": nnz,
+        "mode": args.mode,
+        "preconditioner": "jacobi",
+        "rtol": 1e-5,
+        "truncation": "pod-a-rbf nu_y=1 nu_w=1 storage_cap=60 max_dim=60",
+        "l2": "inputs larger than L2 (780 MB CSR per SpMV); no flush",
+        "parallelism": "replicas (one independent sequence per GPU)",
+    }
+
+
+def solver_config(pk, mode):
+    tr = pk.TruncationConfig(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=60, max_dim=60)
+    return pk.SolverConfig(truncation=tr, mode=mode)
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing (replicas only: no data-path collective)
+# ---------------------------------------------------------------------------
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws <= 1:
+        return 0, 1, None
+    import torch.distributed as dist
+
+    backend = "nccl" if _cuda() else "gloo"
+    dist.init_process_group(backend=backend)
+    return dist.get_rank(), ws, dist
+
+
+def _cuda():
+    import torch
+
+    return torch.cuda.is_available()
+
+
+def max_over_ranks(value: float, dist) -> float:
+    """Max of a per-rank scalar (device timing) over all ranks."""
+    if dist is None:
+        return value
+    import torch
+
+    dev = torch.device("cuda", torch.cuda.current_device()) if _cuda() else torch.device("cpu")
+    t = torch.tensor([value], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling during the timed region
+# ---------------------------------------------------------------------------
+_REASONS = [(0x1, "gpu_idle"), (0x2, "applications_clocks_setting"), (0x4, "sw_power_cap"), (0x8, "hw_slowdown"),
+            (0x20, "sw_thermal_slowdown"), (0x40, "hw_thermal_slowdown"), (0x80, "hw_power_brake_slowdown"),
+            (0x100, "display_clock_setting")]
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,utilization.gpu"
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                f = [x.strip() for x in out.stdout.strip().split(",")]
+                self.samples.append((float(f[0]), float(f[1]), int(f[2], 16) if f[2].startswith("0x") else int(f[2]),
+                                     float(f[3])))
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        loaded = [s for s in self.samples if s[3] > 10] or self.samples
+        reasons = set()
+        for s in loaded:
+            for bit, name in _REASONS:
+                if s[2] & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median([s[0] for s in loaded])), "sm_max_mhz": max(s[1] for s in loaded),
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def spmv_bytes(n, nnz):
+    """Algorithmic bytes of one CSR SpMV: fp64 value + int32 column
+    per nonzero, the int32 row pointer, x read once, y written once."""
+    return 12 * nnz + 4 * (n + 1) + 16 * n
+
+
+def run_b200(args, rank, world, dist):
+    import torch
+
+    import paper_1512_05820_b200 as pk
+    from paper_1512_05820_b200 import _native as nat
+    from paper_1512_05820_b200.problems import elasticity_sequence
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lib = nat.lib()
+    seq = elasticity_sequence((args.grid,) * 3, p=args.systems, rtol=1e-5, seed=3 + rank)
+    host_specs = list(seq)  # host CSR values + rhs for every system (the e2e inputs)
+    n = seq.n
+    nnz = host_specs[0].A.nnz
+    # device-resident inputs for `value`
+    dev_specs = []
+    for s in host_specs:
+        A = pk.SparseSpdMatrix.from_host(s.A)
+        dev_specs.append(pk.LinearSystemSpec(A=A, b=torch.from_numpy(s.b).to(dev), xbar=None, tol=s.tol))
+    dseq = pk.SystemSequence(n, dev_specs, C=seq.C)
+    cfg = solver_config(pk, args.mode)
+    jac = lambda A: pk.build_preconditioner("jacobi", A)  # noqa: E731
+    torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        pk.run_sequence(dseq, cfg, precond_factory=jac)
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    times = []
+    reports = None
+    launches0 = lib.rk_launch_count()
+    lib.rk_profile_begin()
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            barrier(dist)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            xs, reports, _ = pk.run_sequence(dseq, cfg, precond_factory=jac)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+    ms = (ctypes.c_double * 3)()
+    cnt = (ctypes.c_int64 * 3)()
+    lib.rk_profile_end(ms, cnt)
+    launches = (lib.rk_launch_count() - launches0) / max(args.steps, 1)
+    t_step = max_over_ranks(float(np.mean(times)), dist)
+
+    # q = c'x of the last timed sequence (D2H only after timing)
+    q_last = float(seq.C[0] @ xs[-1].cpu().numpy())
+
+    # e2e: the public API from host CSR arrays; H2D of values+rhs and D2H of x inside
+    e2e = None
+    if not args.no_e2e:
+        hseq = pk.SystemSequence(n, host_specs, C=seq.C)
+        h2d = sum(s.A.values.nbytes + s.b.nbytes for s in host_specs)
+        d2h = n * 8 * len(host_specs)
+        barrier(dist)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        xs_e, reps_e, _ = pk.run_sequence(hseq, cfg, precond_factory=jac)
+        xh = [x.cpu().numpy() for x in xs_e]
+        torch.cuda.synchronize()
+        t_e2e = max_over_ranks(time.perf_counter() - t0, dist)
+        e2e = {"value": round(t_e2e / world, 4), "unit": UNIT, "h2d_bytes_per_step": int(h2d * world),
+               "d2h_bytes_per_step": int(d2h * world),
+               "path": "run_sequence over host CSR (reference-style SparseSpdMatrix fields), solutions copied back"}
+        del xh
+
+    avg = [ms[i] / max(cnt[i], 1) for i in range(3)]
+    peaks = _peaks()
+    ach = spmv_bytes(n, nnz) / (avg[0] * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(NCU_SUMMARY) as fh:
+            traffic = json.load(fh).get("k_spmv_pcg", {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    iters = [r.stage3_iters for r in reports]
+    sched = {"stage3_iters": iters, "truncated": [bool(r.truncated) for r in reports],
+             "basis_dim": [r.basis_dim for r in reports], "grown": [r.basis_dim + r.stage3_iters for r in reports]}
+    line = {
+        "metric": METRIC,
+        "value": round(t_step / world, 4),
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(t_step * 1e3, 2),
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded C3 generator, BASELINE configs[2] shapes)",
+        "config": workload_config(args, n, nnz),
+        "roofline": {
+            "kernel": "k_spmv_pcg (K1 CSR SpMV fused with p'Ap, p'p)",
+            "bound": "hbm",
+            "achieved": round(ach, 1),
+            "peak": peaks["hbm_gbs"],
+            "unit": "GB/s",
+            "frac": round(ach / peaks["hbm_gbs"], 3),
+            "traffic": traffic,
+            "algorithmic_bytes_per_launch": spmv_bytes(n, nnz),
+            "avg_launch_ms": round(avg[0], 4),
+            "peak_source": peaks["source"],
+        },
+        "kernels_ms_avg": {"spmv_pcg": round(avg[0], 4), "pcg_update": round(avg[1], 4),
+                           "pcg_direction": round(avg[2], 4), "launches": list(cnt)},
+        "sequence": {"stage3_iters_total": int(sum(iters)), "cg_iters_per_s": round(sum(iters) / t_step, 1),
+                     "per_system_iters": iters, "q_last": q_last,
+                     "all_converged": bool(all(r.converged for r in reports))},
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+    }
+    if rank == 0:
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+        with open(os.path.join(ROOT, "gpurun_out", "c3_schedule.json"), "w") as fh:
+            json.dump(sched, fh)
+    return line, host_specs, sched
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "MEASURED_PEAKS.json (measured copy, burst)"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "source": "fallback 6.65 TB/s (B200_PROFILING.md)"}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle sample, scaled to the metric
+# ---------------------------------------------------------------------------
+def cpu_sample(host_specs, sched, budget_s=20.0):
+    """Time the oracle (numpy/scipy, as the reference) on a bounded sample of
+    the C3 workload and scale it to one sequence with the GPU run's schedule:
+    t = sum_j iters_j * t_iter(m_j) + sum_truncations t_trunc(grown_j)."""
+    import scipy.sparse  # noqa: F401
+
+    from oracle import recycle_oracle as O
+
+    A = O.as_csr(host_specs[0].A)
+    n = A.shape[0]
+    b = host_specs[0].b
+    dinv = 1.0 / A.diagonal()
+    cores = len(os.sched_getaffinity(0))
+    rng = np.random.default_rng(0)
+
+    def iters_cost(Y, k):
+        t = O.Tally()
+        proj = None
+        yh = None
+        if Y is not None:
+            proj = O.assembled_projection(lambda v: O.matvec(A, v, t), Y)
+            yh = np.zeros(Y.shape[1])
+        t0 = time.perf_counter()
+        try:
+            O.aug_pcg(lambda v: O.matvec(A, v, t), b, yh, Y, proj, dinv, 0.0, mode="cg", max_iter=k,
+                      r0=b.copy(), tally=t)
+        except O.OracleNotConverged:
+            pass
+        return (time.perf_counter() - t0) / k
+
+    k0 = 12
+    t_it0 = iters_cost(None, k0)
+    Y = np.linalg.qr(rng.standard_normal((n, 60)))[0]
+    t_it60 = iters_cost(Y, 8)
+    # truncation sample: SpMM + Gram with 32 columns, eigh at full width, S @ coef sample
+    s_cols = 32
+    Z = rng.standard_normal((n, s_cols))
+    t0 = time.perf_counter()
+    AZ = A @ Z
+    t_spmm = (time.perf_counter() - t0) / s_cols
+    t0 = time.perf_counter()
+    _ = Z.T @ AZ
+    t_gram_unit = (time.perf_counter() - t0) / (s_cols * s_cols)
+    grown = max(sched["grown"]) if sched else 760
+    G = rng.standard_normal((grown, grown))
+    G = G + G.T
+    t0 = time.perf_counter()
+    np.linalg.eigh(G)
+    t_evd = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    _ = Z @ rng.standard_normal((s_cols, 60))
+    t_rec_unit = (time.perf_counter() - t0) / s_cols
+
+    total = 0.0
+    if sched:
+        for j, (k, g) in enumerate(zip(sched["stage3_iters"], sched["grown"])):
+            total += k * (t_it0 if j == 0 else t_it60)
+            if j > 0:
+                total += 60 * t_spmm + 60 * 60 * t_gram_unit      # stage-1 assemble_gram of W
+            total += g * t_spmm + g * g * t_gram_unit + t_evd * (g / grown) ** 3 + g * t_rec_unit
+    return {
+        "value": round(total, 2),
+        "unit": UNIT,
+        "cores": cores,
+        "kind": "port",
+        "sample": (f"oracle on C3 system 1: {k0} plain PCG iterations ({t_it0*1e3:.0f} ms/it), 8 iterations "
+                   f"projected against 60 columns ({t_it60*1e3:.0f} ms/it), a {s_cols}-column SpMM+Gram, "
+                   f"S@coef and eigh({grown}); scaled to the sequence with the GPU run's schedule "
+                   f"({sum(sched['stage3_iters']) if sched else 0} stage-3 iterations, extrapolated)"),
+        "components_s": {"t_iter_plain": t_it0, "t_iter_m60": t_it60, "t_spmm_per_col": t_spmm,
+                         "t_gram_per_col2": t_gram_unit, "t_evd_full": t_evd},
+    }
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle port on the box's host cores (rank 0 only)."""
+    if rank != 0:
+        return None
+    from paper_1512_05820_b200.problems import elasticity_sequence
+
+    seq = elasticity_sequence((args.grid,) * 3, p=min(args.systems, 1), rtol=1e-5, seed=3)
+    host_specs = list(seq)
+    sched = None
+    try:
+        with open(SCHEDULE) as fh:
+            sched = json.load(fh)
+    except Exception:
+        sched = None
+    vals = []
+    for _ in range(args.warmup):
+        cpu_sample(host_specs, sched)
+    for _ in range(args.steps):
+        cb = cpu_sample(host_specs, sched)
+        vals.append(cb["value"])
+    v = float(np.mean(vals))
+    cb["value"] = round(v, 2)
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": round(v, 2),
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded C3 generator, BASELINE configs[2] shapes)",
+        "config": workload_config(args, seq.n, host_specs[0].A.nnz),
+        "cpu_baseline": cb,
+        "e2e": {"value": round(v, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": ("reference = pure-Python numpy/scipy (recykl); timed through its restatement oracle/recycle_oracle.py "
+                 "on a bounded sample and scaled with profiles/c3_schedule.json (extrapolated)"),
+    }
+    return line
+
+
+def main():
+    args = parse()
+    rank, world, dist = dist_init()
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+        if rank == 0 and line is not None:
+            print(json.dumps(line))
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    line, host_specs, sched = run_b200(args, rank, world, dist)
+    if rank == 0:
+        if world == 1 and not args.no_cpu:
+            line["cpu_baseline"] = cpu_sample(host_specs, sched)
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -174,6 +174,12 @@ _pattern_cache_lock = threading.Lock()
 _pattern_cache: list = []  # [(host rowptr, host col, device rowptr, device col)]
 
 
+def _pattern_known(rowptr: np.ndarray, col: np.ndarray, device) -> bool:
+    """Same host pattern objects already uploaded (and checked) for this device."""
+    with _pattern_cache_lock:
+        return any(dr.device == device and hr is rowptr and hc is col for hr, hc, dr, dc in _pattern_cache)
+
+
 def _device_pattern(rowptr: np.ndarray, col: np.ndarray, device):
     with _pattern_cache_lock:
         for hr, hc, dr, dc in _pattern_cache:
@@ -218,7 +224,7 @@ class SparseSpdMatrix:
                 raise DimensionMismatch(
                     f"row_offsets must have length n+1={self.n + 1}, got {rp_h.shape}"
                 )
-            if ci_h.size and (not _rows_sorted(rp_h, ci_h)):
+            if ci_h.size and not _pattern_known(rp_h, ci_h, self.device) and not _rows_sorted(rp_h, ci_h):
                 csr = scipy.sparse.csr_matrix(
                     (np.asarray(values, dtype=np.float64), ci_h, rp_h), shape=(self.n, self.n)
                 )
