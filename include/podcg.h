@@ -177,6 +177,14 @@ int rk_sub_from(int64_t n, const double* x0, double* y, void* stream);
 int rk_gram(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m2,
             const double* Y, int64_t ldy, double* G, int64_t ldg, double* ws,
             int64_t ws_len, void* stream);
+/* Upper-triangle variant for a block G = X'Y of a symmetric matrix whose column b
+ * is global column b + col_off (row a is global row a): 64x64 tiles strictly below
+ * the diagonal are skipped and left undefined; the caller mirrors the upper part.
+ * Halves the flops of the POD snapshot Gram S'(AS) (pod.py:119, symmetrised by
+ * the reference at pod.py:129 anyway). */
+int rk_gram_upper(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m2,
+                  const double* Y, int64_t ldy, int64_t col_off, double* G, int64_t ldg,
+                  double* ws, int64_t ws_len, void* stream);
 /* Out (N x y) = S (N x s) C (s x y) (pod.py:91-93 `S @ coef`). */
 int rk_gemm_nn(int64_t n, int64_t s, int64_t y, const double* S, int64_t lds,
                const double* C, int64_t ldc, double* Out, int64_t ldo, void* stream);

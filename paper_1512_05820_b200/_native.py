@@ -117,6 +117,8 @@ _SIGNATURES = {
     "rk_axpby": (c_i32, [c_i64, c_dbl, c_vp, c_dbl, c_vp, c_vp]),
     "rk_sub_from": (c_i32, [c_i64, c_vp, c_vp, c_vp]),
     "rk_gram": (c_i32, [c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp]),
+    "rk_gram_upper": (c_i32, [c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64,
+                              c_vp]),
     "rk_gemm_nn": (c_i32, [c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp]),
     "rk_profile_begin": (c_i32, []),
     "rk_launch_count": (c_i64, []),

@@ -43,12 +43,16 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 __global__ void __launch_bounds__(kDmmaThreads, 2)
     k_gram(int64_t n, int64_t m1, const double* __restrict__ X, int64_t ldx, int64_t m2,
            const double* __restrict__ Y, int64_t ldy, double* __restrict__ out, int64_t ldo,
-           int64_t split_stride, int64_t rows_per_split) {
+           int64_t split_stride, int64_t rows_per_split, int64_t upper_off) {
   extern __shared__ __align__(16) double smem[];
   double* Xs = smem;                                  // [stage][a][kPadK]
   double* Ys = smem + kStages * kTile * kPadK;        // [stage][b][kPadK]
   const int64_t a0 = (int64_t)blockIdx.x * kTile;
   const int64_t b0 = (int64_t)blockIdx.y * kTile;
+  // upper mode: G is a block of a symmetric matrix whose column b sits at global
+  // column b + upper_off; tiles strictly below the diagonal are skipped (their
+  // entries are left undefined and mirrored by the caller).
+  if (upper_off >= 0 && a0 > b0 + upper_off + kTile - 1) return;
   const int64_t kbeg = (int64_t)blockIdx.z * rows_per_split;
   const int64_t kend = min(n, kbeg + rows_per_split);
   const int nsteps = kend > kbeg ? (int)((kend - kbeg + kStep - 1) / kStep) : 0;
@@ -261,7 +265,7 @@ int64_t gram_workspace_doubles(int64_t n, int64_t m1, int64_t m2) {
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
 int launch_gram(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m2, const double* Y, int64_t ldy,
-                double* G, int64_t ldg, double* ws, int64_t ws_len, cudaStream_t s) {
+                double* G, int64_t ldg, double* ws, int64_t ws_len, int64_t upper_off, cudaStream_t s) {
   if (m1 <= 0 || m2 <= 0) return 0;
   RK_REQUIRE(aligned16(X) && aligned16(Y) && (ldx % 2 == 0) && (ldy % 2 == 0), RK_ERR_ARG,
              "rk_gram: operands need 16-byte aligned columns with even leading dimension");
@@ -274,12 +278,13 @@ int launch_gram(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m2,
   const GramGeom g = gram_geometry(std::max<int64_t>(n, 1), m1, m2);
   dim3 grid((unsigned)g.ta, (unsigned)g.tb, (unsigned)g.splits);
   if (g.splits == 1) {
-    rk::k_gram<<<grid, rk::kDmmaThreads, gram_smem(), s>>>(n, m1, X, ldx, m2, Y, ldy, G, ldg, 0, g.rows_per_split); rkh::note_launch();
+    rk::k_gram<<<grid, rk::kDmmaThreads, gram_smem(), s>>>(n, m1, X, ldx, m2, Y, ldy, G, ldg, 0, g.rows_per_split,
+                                                           upper_off); rkh::note_launch();
   } else {
     RK_REQUIRE(ws && ws_len >= g.splits * m1 * m2, RK_ERR_ARG, "rk_gram: workspace too small (%lld < %lld)",
                (long long)ws_len, (long long)(g.splits * m1 * m2));
     rk::k_gram<<<grid, rk::kDmmaThreads, gram_smem(), s>>>(n, m1, X, ldx, m2, Y, ldy, ws, m1, m1 * m2,
-                                                            g.rows_per_split); rkh::note_launch();
+                                                            g.rows_per_split, upper_off); rkh::note_launch();
     const int64_t total = m1 * m2;
     const int rg = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 8));
     rk::k_gram_reduce<<<rg, 256, 0, s>>>(m1, m2, g.splits, ws, G, ldg); rkh::note_launch();

@@ -44,26 +44,39 @@ constexpr int kRows = 4;                          // rows per thread per chunk
 constexpr int kUpdChunk = kUpdThreads * kRows;    // rows per chunk
 constexpr int kColGroup = 8;                      // cross columns reduced together
 constexpr int kMaxProj = 4096;    // projection width supported by the fused path
+constexpr int kMaxStagedChol = 96;  // dense factor staged in smem up to this width
 
 // mu = F^{-1} c with F = blockdiag(L L', diag(sqd)^2): forward and back
 // substitution on the dense block (one warp), division on the diagonal block
 // (krylov.py:119-132 BlockDiagFactor.solve_spd).
-__device__ void solve_factor(const rk_pcg_plan& P, const double* c, double* ysm, double* mu) {
+__device__ void solve_factor(const rk_pcg_plan& P, const double* c, double* ysm, double* Ls, double* mu) {
   const int lane = threadIdx.x & 31;
   const int64_t w = P.wchol, m = P.m;
+  // Stage the dense factor in shared memory first: the substitutions are a
+  // chain of w dependent steps, and each step must not wait on L2.
+  const bool staged = w <= kMaxStagedChol;
+  const double* L = staged ? Ls : P.L;
+  const int64_t ldl = staged ? w : P.ldl;
+  if (staged) {
+    for (int64_t e = threadIdx.x; e < w * w; e += blockDim.x) {
+      const int64_t i = e % w, j = e / w;
+      Ls[e] = (i >= j) ? P.L[i + j * P.ldl] : 0.0;
+    }
+    __syncthreads();
+  }
   if (threadIdx.x < 32) {
     for (int64_t i = 0; i < w; ++i) {
       double s = 0.0;
-      for (int64_t j = lane; j < i; j += 32) s = fma(P.L[i + j * P.ldl], ysm[j], s);
+      for (int64_t j = lane; j < i; j += 32) s = fma(L[i + j * ldl], ysm[j], s);
       s = warp_sum(s);
-      if (lane == 0) ysm[i] = (c[i] - s) / P.L[i + i * P.ldl];
+      if (lane == 0) ysm[i] = (c[i] - s) / L[i + i * ldl];
       __syncwarp();
     }
     for (int64_t i = w - 1; i >= 0; --i) {
       double s = 0.0;
-      for (int64_t j = i + 1 + lane; j < w; j += 32) s = fma(P.L[j + i * P.ldl], ysm[j + w], s);
+      for (int64_t j = i + 1 + lane; j < w; j += 32) s = fma(L[j + i * ldl], ysm[j + w], s);
       s = warp_sum(s);
-      if (lane == 0) ysm[i + w] = (ysm[i] - s) / P.L[i + i * P.ldl];
+      if (lane == 0) ysm[i + w] = (ysm[i] - s) / L[i + i * ldl];
       __syncwarp();
     }
   }
@@ -98,7 +111,107 @@ __global__ void __launch_bounds__(kUpdThreads) k_pcg_update(const rk_pcg_plan P,
   for (int64_t j = threadIdx.x; j < 2 + m; j += blockDim.x) red[j] = 0.0;
   double acc[2] = {0.0, 0.0};
   const int64_t nchunks = (n + kUpdChunk - 1) / kUpdChunk;
-  for (int64_t chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
+  // Fast path: whole 1024-row chunks with 16-byte vector accesses, every load
+  // of a stage issued before its first use (vectors and the columns of cross
+  // are 256-byte aligned by the host layer). Each thread owns rows
+  // base + 2*(u*256 + tid) + {0, 1}, u = 0, 1.
+  const bool vec_ok = ((P.ldc & 1) == 0) && (((uintptr_t)p | (uintptr_t)Ap | (uintptr_t)x | (uintptr_t)r |
+                                              (uintptr_t)z | (uintptr_t)dinv | (uintptr_t)cross) & 15) == 0;
+  const int64_t nfull = vec_ok ? n / kUpdChunk : 0;
+  for (int64_t chunk = blockIdx.x; chunk < nfull; chunk += gridDim.x) {
+    const int64_t base = chunk * kUpdChunk;
+    double2 rv[2], dv[2], xv[2], pv[2], av[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t q = (base >> 1) + u * kUpdThreads + threadIdx.x;  // double2 index
+      rv[u] = reinterpret_cast<const double2*>(r)[q];
+      dv[u] = dinv ? __ldg(reinterpret_cast<const double2*>(dinv) + q) : make_double2(1.0, 1.0);
+      if (!entry) {
+        xv[u] = reinterpret_cast<const double2*>(x)[q];
+        pv[u] = reinterpret_cast<const double2*>(p)[q];
+        av[u] = reinterpret_cast<const double2*>(Ap)[q];
+      }
+    }
+    double zr[4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t q = (base >> 1) + u * kUpdThreads + threadIdx.x;
+      double r0 = rv[u].x, r1 = rv[u].y;
+      if (!entry) {
+        // krylov.py:306-307  x = x + alpha * p ; r = r - alpha * Ap
+        reinterpret_cast<double2*>(x)[q] =
+            make_double2(__dadd_rn(xv[u].x, __dmul_rn(alpha, pv[u].x)), __dadd_rn(xv[u].y, __dmul_rn(alpha, pv[u].y)));
+        r0 = __dsub_rn(r0, __dmul_rn(alpha, av[u].x));
+        r1 = __dsub_rn(r1, __dmul_rn(alpha, av[u].y));
+        reinterpret_cast<double2*>(r)[q] = make_double2(r0, r1);
+      }
+      // preconditioners.py:61  r * inv_diag  (identity: r.copy())
+      const double z0 = dinv ? __dmul_rn(r0, dv[u].x) : r0;
+      const double z1 = dinv ? __dmul_rn(r1, dv[u].y) : r1;
+      reinterpret_cast<double2*>(z)[q] = make_double2(z0, z1);
+      zr[2 * u] = z0;
+      zr[2 * u + 1] = z1;
+      acc[0] = fma(r0, r0, acc[0]);
+      acc[0] = fma(r1, r1, acc[0]);
+      acc[1] = fma(r0, z0, acc[1]);
+      acc[1] = fma(r1, z1, acc[1]);
+    }
+    // K4 on the chunk: 8 columns of cross at a time, 16 independent 16-byte
+    // loads per thread in flight, then a fixed-order block reduction.
+    for (int64_t j0 = 0; j0 < m; j0 += kColGroup) {
+      double a[kColGroup];
+      if (j0 + kColGroup <= m) {
+        double2 cv[kColGroup][2];
+#pragma unroll
+        for (int c = 0; c < kColGroup; ++c)
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+            cv[c][u] = __ldcs(reinterpret_cast<const double2*>(cross + (j0 + c) * P.ldc + base) + u * kUpdThreads +
+                              threadIdx.x);
+#pragma unroll
+        for (int c = 0; c < kColGroup; ++c) {
+          double t = 0.0;
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            t = fma(cv[c][u].x, zr[2 * u], t);
+            t = fma(cv[c][u].y, zr[2 * u + 1], t);
+          }
+          a[c] = t;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < kColGroup; ++c) {
+          double t = 0.0;
+          if (j0 + c < m) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const double2 v = __ldcs(reinterpret_cast<const double2*>(cross + (j0 + c) * P.ldc + base) +
+                                       u * kUpdThreads + threadIdx.x);
+              t = fma(v.x, zr[2 * u], t);
+              t = fma(v.y, zr[2 * u + 1], t);
+            }
+          }
+          a[c] = t;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < kColGroup; ++c) a[c] = warp_sum(a[c]);
+      if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < kColGroup; ++c) wsum[warp * kColGroup + c] = a[c];
+      }
+      __syncthreads();
+      if (threadIdx.x < kColGroup && j0 + threadIdx.x < m) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < kUpdThreads / 32; ++w) t += wsum[w * kColGroup + threadIdx.x];
+        red[2 + j0 + threadIdx.x] += t;
+      }
+      __syncthreads();
+    }
+  }
+  // Generic path: the tail chunk (and unaligned operands), scalar and predicated.
+  for (int64_t chunk = nfull + blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
     const int64_t i0 = chunk * kUpdChunk + threadIdx.x;
     // K3: R rows per thread, all loads issued before use (stride = block size,
     // so each of the R passes is a fully coalesced warp access)
@@ -201,7 +314,7 @@ __global__ void __launch_bounds__(kUpdThreads) k_pcg_update(const rk_pcg_plan P,
   __syncthreads();
   if (s_stop || m == 0) return;
   double* ysm = red + nv;  // 2*wchol scratch
-  solve_factor(P, red + 2, ysm, P.mu);
+  solve_factor(P, red + 2, ysm, ysm + 2 * P.wchol, P.mu);
 }
 
 // K5: new direction into V[:, k+1] (entry: V[:, 0]).
@@ -269,7 +382,7 @@ struct UpdGeom {
 static UpdGeom update_geometry(int64_t n, int64_t m, int64_t wchol) {
   UpdGeom g;
   const int64_t nchunks = (n + rk::kUpdChunk - 1) / rk::kUpdChunk;
-  g.smem = (size_t)(2 + m + 2 * wchol) * sizeof(double);
+  g.smem = (size_t)(2 + m + 2 * wchol + (wchol <= rk::kMaxStagedChol ? wchol * wchol : 0)) * sizeof(double);
   // one resident wave; chunks are grid-strided so every block does equal work
   static int occ = [] {
     int o = 0;

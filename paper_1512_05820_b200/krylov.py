@@ -382,13 +382,16 @@ def augmented_pcg(
     r0=None,
     monitor=None,
     batch: int | None = None,
+    keep_products: bool = False,
 ) -> AugmentedPcgResult:
     """Augmented PCG over the affine space Y yhat0 + directions (krylov.py:181-345).
 
     Same parameters, exceptions (``NotConverged`` with the partial result,
     ``Breakdown``, ``DimensionMismatch``, ``ValueError`` for an unknown mode)
     and sink accounting as the reference. ``batch`` caps the number of
-    iterations launched between host checks on the fused path.
+    iterations launched between host checks on the fused path;
+    ``keep_products`` keeps every A p_k as a column of ``result.AV`` (fom mode
+    keeps them anyway) so a later POD truncation needs no SpMM.
     """
     operator = _as_operator(op, sink)
     n = int(operator.dim)
@@ -423,7 +426,7 @@ def augmented_pcg(
         code = 2
     direct = isinstance(reduced_solver, DirectReducedProjection)
     m = int(Y.shape[1]) if Y is not None else 0
-    keep_av = code == 1
+    keep_av = code == 1 or keep_products
     max_iter = n if max_iter is None else int(max_iter)
     run = _Run(n, device, max(code, 0), keep_av, m if direct else 0, vcap=min(max_iter + 2, 64))
 
@@ -507,9 +510,11 @@ def _count_matvecs(operator, count):
 
 def _result(run: _Run, k: int, converged: bool) -> AugmentedPcgResult:
     alphas, gammas, hist = run.histories(k)
-    return AugmentedPcgResult(
+    res = AugmentedPcgResult(
         k=k, vhat=alphas, V=run.V[:, :k], gamma=gammas, residual_history=hist, x=run.x, converged=converged
     )
+    res.AV = run.AV[:, :k] if run.keep_av else None  # A p_k columns (same operator as the run)
+    return res
 
 
 def _drive_fused(run: _Run, max_iter: int, batch: int | None):

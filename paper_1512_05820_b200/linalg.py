@@ -414,6 +414,35 @@ def gram(X: torch.Tensor, Y: torch.Tensor) -> torch.Tensor:
     return G
 
 
+def symmetric_gram_from_products(Z: torch.Tensor, products, col_scale=None) -> np.ndarray:
+    """Host copy of the symmetric Z'AZ from cached products A Z.
+
+    ``products`` is a list of (AZ_block, col_off): AZ_block holds A applied to
+    columns [col_off, col_off + w) of Z (e.g. the stage-1 product A W and the
+    stored A p_k of the PCG run). Only the upper 64x64 tiles are computed on the
+    device (rk_gram_upper) and mirrored here; ``col_scale`` (length m or None)
+    rescales column j afterwards (products of unscaled directions)."""
+    n, m = Z.shape
+    dev = Z.device
+    store = torch.zeros((max(m, 1), max(m, 1)), dtype=F64, device=dev)  # column-major m x m (ld = m)
+    s = nat.scratch(dev)
+    for AB, off in products:
+        w = int(AB.shape[1])
+        if w == 0:
+            continue
+        ws = s.workspace(max(nat.lib().rk_gram_workspace_doubles(n, m, w), 1))
+        Gblk = store[off : off + w]  # rows of the row-major store = columns of G
+        nat.check(nat.lib().rk_gram_upper(n, m, Z.data_ptr(), block_ld(Z), w, AB.data_ptr(), block_ld(AB), off,
+                                          Gblk.data_ptr(), m, ws.data_ptr(), ws.numel(), nat.stream_ptr(dev)),
+                  "gram_upper")
+    G = store[:m, :m].cpu().numpy().T.copy()  # G[a, b] with a row, b column
+    if col_scale is not None:
+        G = G * np.asarray(col_scale, dtype=np.float64)[None, :]
+    iu = np.triu_indices(m, 1)
+    G[(iu[1], iu[0])] = G[iu]
+    return G
+
+
 def gemm_nn(S: torch.Tensor, C, out: torch.Tensor | None = None) -> torch.Tensor:
     """S (N x s) @ C (s x y) with the DMMA kernel (pod.py:91-93)."""
     n, s = S.shape
