@@ -81,7 +81,8 @@ typedef struct rk_pcg_plan {
   int64_t n;
   rk_csr A;                 /* A.rowptr == NULL: generic operator, caller fills AV */
   double* x;
-  double* r;
+  double* r;                /* residual buffer 0 (holds r_0 at entry) */
+  double* r2;               /* residual buffer 1: iteration k reads buffer k&1, writes the other */
   double* z;
   double* V;                /* directions, column k = p_k */
   int64_t ldv;
@@ -94,7 +95,8 @@ typedef struct rk_pcg_plan {
   int64_t ldb;
   const double* cross;      /* cached A*B, N x m (DirectReducedProjection.cross) */
   int64_t ldc;
-  const double* L;          /* dense lower Cholesky factor of the leading wchol block */
+  const double* L;          /* Linv = L^{-1}, inverse of the lower Cholesky factor of the
+                               leading wchol block (host dtrtri), lower triangular */
   int64_t ldl;
   int64_t wchol;
   const double* sqd;        /* sqrt-diagonal factor blocks for rows wchol..m-1 */

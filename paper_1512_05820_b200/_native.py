@@ -62,6 +62,7 @@ class RkPcgPlan(ctypes.Structure):
         ("A", RkCsr),
         ("x", c_vp),
         ("r", c_vp),
+        ("r2", c_vp),
         ("z", c_vp),
         ("V", c_vp),
         ("ldv", c_i64),

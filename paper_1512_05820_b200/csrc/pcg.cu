@@ -40,45 +40,37 @@ int elementwise_grid(int64_t n);
 namespace rk {
 
 constexpr int kUpdThreads = 256;
-constexpr int kRows = 4;                          // rows per thread per chunk
-constexpr int kUpdChunk = kUpdThreads * kRows;    // rows per chunk
-constexpr int kColGroup = 8;                      // cross columns reduced together
-constexpr int kMaxProj = 4096;    // projection width supported by the fused path
-constexpr int kMaxStagedChol = 96;  // dense factor staged in smem up to this width
+constexpr int kProjChunk = 1024;                 // rows per update block
+constexpr int kProjCols = 32;                    // cross columns per update block (4 per warp)
+constexpr int kMaxProj = 2048;                   // projection width of the fused path
+constexpr int kMaxStagedChol = 96;               // dense factor staged in smem up to this width
 
-// mu = F^{-1} c with F = blockdiag(L L', diag(sqd)^2): forward and back
-// substitution on the dense block (one warp), division on the diagonal block
-// (krylov.py:119-132 BlockDiagFactor.solve_spd).
+// mu = F^{-1} c with F = blockdiag(L L', diag(sqd)^2) (krylov.py:119-132
+// BlockDiagFactor.solve_spd). P.L holds Linv = L^{-1} (lower triangular, from
+// LAPACK dtrtri on the host), so the two triangular solves become two
+// triangular mat-vecs, y = Linv c and mu = Linv' y, one output per thread
+// (instead of a chain of w dependent substitution steps); the diagonal block
+// is a division.
 __device__ void solve_factor(const rk_pcg_plan& P, const double* c, double* ysm, double* Ls, double* mu) {
-  const int lane = threadIdx.x & 31;
   const int64_t w = P.wchol, m = P.m;
-  // Stage the dense factor in shared memory first: the substitutions are a
-  // chain of w dependent steps, and each step must not wait on L2.
   const bool staged = w <= kMaxStagedChol;
   const double* L = staged ? Ls : P.L;
   const int64_t ldl = staged ? w : P.ldl;
   if (staged) {
-    for (int64_t e = threadIdx.x; e < w * w; e += blockDim.x) {
-      const int64_t i = e % w, j = e / w;
-      Ls[e] = (i >= j) ? P.L[i + j * P.ldl] : 0.0;
-    }
+    for (int64_t j = 0; j < w; ++j)
+      for (int64_t i = threadIdx.x; i < w; i += blockDim.x) Ls[i + j * w] = (i >= j) ? P.L[i + j * P.ldl] : 0.0;
     __syncthreads();
   }
-  if (threadIdx.x < 32) {
-    for (int64_t i = 0; i < w; ++i) {
-      double s = 0.0;
-      for (int64_t j = lane; j < i; j += 32) s = fma(L[i + j * ldl], ysm[j], s);
-      s = warp_sum(s);
-      if (lane == 0) ysm[i] = (c[i] - s) / L[i + i * ldl];
-      __syncwarp();
-    }
-    for (int64_t i = w - 1; i >= 0; --i) {
-      double s = 0.0;
-      for (int64_t j = i + 1 + lane; j < w; j += 32) s = fma(L[j + i * ldl], ysm[j + w], s);
-      s = warp_sum(s);
-      if (lane == 0) ysm[i + w] = (ysm[i] - s) / L[i + i * ldl];
-      __syncwarp();
-    }
+  for (int64_t i = threadIdx.x; i < w; i += blockDim.x) {   // y = Linv c
+    double s = 0.0;
+    for (int64_t j = 0; j <= i; ++j) s = fma(L[i + j * ldl], c[j], s);
+    ysm[i] = s;
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < w; i += blockDim.x) {   // mu = Linv' y
+    double s = 0.0;
+    for (int64_t j = i; j < w; ++j) s = fma(L[j + i * ldl], ysm[j], s);
+    ysm[i + w] = s;
   }
   __syncthreads();
   for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
@@ -90,203 +82,144 @@ __device__ void solve_factor(const rk_pcg_plan& P, const double* c, double* ysm,
   }
 }
 
+// Residual ping-pong: iteration k reads r_k from buffer k&1 and writes r_{k+1}
+// to the other one, so every block of the 2-D update grid can recompute z for
+// its rows from unmodified inputs (entry reads buffer 0 and writes nothing).
+__device__ __forceinline__ const double* r_in(const rk_pcg_plan& P, int64_t k, int entry) {
+  return (entry || !(k & 1)) ? P.r : P.r2;
+}
+__device__ __forceinline__ double* r_out(const rk_pcg_plan& P, int64_t k) { return (k & 1) ? P.r : P.r2; }
+
+// K3 + K4 partials. Grid (row chunks, column groups of 32). Every block forms
+// z = D^{-1}(r - alpha Ap) for its 1024 rows in shared memory; column group 0
+// also writes x, r_{k+1}, z and the ||r||^2, r'z partials. Then each warp
+// reduces 4 columns of cross' z over the chunk (lanes over rows, 16-byte
+// loads, 16 in flight per lane). Partials: part[v * nchunks + chunk].
 __global__ void __launch_bounds__(kUpdThreads) k_pcg_update(const rk_pcg_plan P, int entry) {
   rk_pcg_state* st = P.st;
   if (st->done) return;
-  extern __shared__ double dyn[];
-  double* red = dyn;                                  // 2 + m running block sums, then 2*wchol scratch
+  __shared__ __align__(16) double zs[kProjChunk];
   __shared__ double scratch[64];
-  __shared__ double wsum[(kUpdThreads / 32) * kColGroup];
   const int64_t k = st->k;
   const double alpha = entry ? 0.0 : st->alpha;
   const int64_t n = P.n, m = P.m;
-  const double* __restrict__ p = P.V + k * P.ldv;
-  const double* __restrict__ Ap = P.AV + (P.ldav ? k * P.ldav : 0);
-  double* __restrict__ x = P.x;
-  double* __restrict__ r = P.r;
-  double* __restrict__ z = P.z;
-  const double* __restrict__ dinv = P.dinv;
-  const double* __restrict__ cross = P.cross;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int64_t j = threadIdx.x; j < 2 + m; j += blockDim.x) red[j] = 0.0;
+  const int64_t nchunks = gridDim.x;
+  const int64_t chunk = blockIdx.x;
+  const int64_t beg = chunk * kProjChunk;
+  const int rows = (int)min((int64_t)kProjChunk, n - beg);
+  const bool lead = blockIdx.y == 0;
+  const double* __restrict__ p = P.V + k * P.ldv + beg;
+  const double* __restrict__ Ap = P.AV + (P.ldav ? k * P.ldav : 0) + beg;
+  const double* __restrict__ rin = r_in(P, k, entry) + beg;
+  double* __restrict__ rout = r_out(P, k) + beg;
+  double* __restrict__ x = P.x + beg;
+  double* __restrict__ z = P.z + beg;
+  const double* __restrict__ dinv = P.dinv ? P.dinv + beg : nullptr;
   double acc[2] = {0.0, 0.0};
-  const int64_t nchunks = (n + kUpdChunk - 1) / kUpdChunk;
-  // Fast path: whole 1024-row chunks with 16-byte vector accesses, every load
-  // of a stage issued before its first use (vectors and the columns of cross
-  // are 256-byte aligned by the host layer). Each thread owns rows
-  // base + 2*(u*256 + tid) + {0, 1}, u = 0, 1.
-  const bool vec_ok = ((P.ldc & 1) == 0) && (((uintptr_t)p | (uintptr_t)Ap | (uintptr_t)x | (uintptr_t)r |
-                                              (uintptr_t)z | (uintptr_t)dinv | (uintptr_t)cross) & 15) == 0;
-  const int64_t nfull = vec_ok ? n / kUpdChunk : 0;
-  for (int64_t chunk = blockIdx.x; chunk < nfull; chunk += gridDim.x) {
-    const int64_t base = chunk * kUpdChunk;
-    double2 rv[2], dv[2], xv[2], pv[2], av[2];
+  constexpr int R = kProjChunk / kUpdThreads;
+  double rv[R], av[R], dv[R], xv[R], pv[R];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int64_t q = (base >> 1) + u * kUpdThreads + threadIdx.x;  // double2 index
-      rv[u] = reinterpret_cast<const double2*>(r)[q];
-      dv[u] = dinv ? __ldg(reinterpret_cast<const double2*>(dinv) + q) : make_double2(1.0, 1.0);
-      if (!entry) {
-        xv[u] = reinterpret_cast<const double2*>(x)[q];
-        pv[u] = reinterpret_cast<const double2*>(p)[q];
-        av[u] = reinterpret_cast<const double2*>(Ap)[q];
-      }
-    }
-    double zr[4];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int64_t q = (base >> 1) + u * kUpdThreads + threadIdx.x;
-      double r0 = rv[u].x, r1 = rv[u].y;
-      if (!entry) {
-        // krylov.py:306-307  x = x + alpha * p ; r = r - alpha * Ap
-        reinterpret_cast<double2*>(x)[q] =
-            make_double2(__dadd_rn(xv[u].x, __dmul_rn(alpha, pv[u].x)), __dadd_rn(xv[u].y, __dmul_rn(alpha, pv[u].y)));
-        r0 = __dsub_rn(r0, __dmul_rn(alpha, av[u].x));
-        r1 = __dsub_rn(r1, __dmul_rn(alpha, av[u].y));
-        reinterpret_cast<double2*>(r)[q] = make_double2(r0, r1);
-      }
-      // preconditioners.py:61  r * inv_diag  (identity: r.copy())
-      const double z0 = dinv ? __dmul_rn(r0, dv[u].x) : r0;
-      const double z1 = dinv ? __dmul_rn(r1, dv[u].y) : r1;
-      reinterpret_cast<double2*>(z)[q] = make_double2(z0, z1);
-      zr[2 * u] = z0;
-      zr[2 * u + 1] = z1;
-      acc[0] = fma(r0, r0, acc[0]);
-      acc[0] = fma(r1, r1, acc[0]);
-      acc[1] = fma(r0, z0, acc[1]);
-      acc[1] = fma(r1, z1, acc[1]);
-    }
-    // K4 on the chunk: 8 columns of cross at a time, 16 independent 16-byte
-    // loads per thread in flight, then a fixed-order block reduction.
-    for (int64_t j0 = 0; j0 < m; j0 += kColGroup) {
-      double a[kColGroup];
-      if (j0 + kColGroup <= m) {
-        double2 cv[kColGroup][2];
-#pragma unroll
-        for (int c = 0; c < kColGroup; ++c)
-#pragma unroll
-          for (int u = 0; u < 2; ++u)
-            cv[c][u] = __ldcs(reinterpret_cast<const double2*>(cross + (j0 + c) * P.ldc + base) + u * kUpdThreads +
-                              threadIdx.x);
-#pragma unroll
-        for (int c = 0; c < kColGroup; ++c) {
-          double t = 0.0;
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            t = fma(cv[c][u].x, zr[2 * u], t);
-            t = fma(cv[c][u].y, zr[2 * u + 1], t);
-          }
-          a[c] = t;
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < kColGroup; ++c) {
-          double t = 0.0;
-          if (j0 + c < m) {
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              const double2 v = __ldcs(reinterpret_cast<const double2*>(cross + (j0 + c) * P.ldc + base) +
-                                       u * kUpdThreads + threadIdx.x);
-              t = fma(v.x, zr[2 * u], t);
-              t = fma(v.y, zr[2 * u + 1], t);
-            }
-          }
-          a[c] = t;
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < kColGroup; ++c) a[c] = warp_sum(a[c]);
-      if (lane == 0) {
-#pragma unroll
-        for (int c = 0; c < kColGroup; ++c) wsum[warp * kColGroup + c] = a[c];
-      }
-      __syncthreads();
-      if (threadIdx.x < kColGroup && j0 + threadIdx.x < m) {
-        double t = 0.0;
-#pragma unroll
-        for (int w = 0; w < kUpdThreads / 32; ++w) t += wsum[w * kColGroup + threadIdx.x];
-        red[2 + j0 + threadIdx.x] += t;
-      }
-      __syncthreads();
-    }
+  for (int u = 0; u < R; ++u) {
+    const int i = u * kUpdThreads + threadIdx.x;
+    const bool ok = i < rows;
+    rv[u] = ok ? rin[i] : 0.0;
+    dv[u] = (ok && dinv) ? __ldg(dinv + i) : 1.0;
+    av[u] = (ok && !entry) ? Ap[i] : 0.0;
+    xv[u] = (ok && !entry && lead) ? x[i] : 0.0;
+    pv[u] = (ok && !entry && lead) ? p[i] : 0.0;
   }
-  // Generic path: the tail chunk (and unaligned operands), scalar and predicated.
-  for (int64_t chunk = nfull + blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
-    const int64_t i0 = chunk * kUpdChunk + threadIdx.x;
-    // K3: R rows per thread, all loads issued before use (stride = block size,
-    // so each of the R passes is a fully coalesced warp access)
-    double xv[kRows], pv[kRows], rv[kRows], av[kRows], dv[kRows], zr[kRows];
 #pragma unroll
-    for (int u = 0; u < kRows; ++u) {
-      const int64_t i = i0 + (int64_t)u * kUpdThreads;
-      const bool ok = i < n;
-      rv[u] = ok ? r[i] : 0.0;
-      dv[u] = (ok && dinv) ? __ldg(dinv + i) : 1.0;
-      if (!entry) {
-        xv[u] = ok ? x[i] : 0.0;
-        pv[u] = ok ? p[i] : 0.0;
-        av[u] = ok ? Ap[i] : 0.0;
-      }
+  for (int u = 0; u < R; ++u) {
+    const int i = u * kUpdThreads + threadIdx.x;
+    if (i >= rows) {
+      zs[i] = 0.0;
+      continue;
     }
-#pragma unroll
-    for (int u = 0; u < kRows; ++u) {
-      const int64_t i = i0 + (int64_t)u * kUpdThreads;
-      zr[u] = 0.0;
-      if (i >= n) continue;
-      double ri = rv[u];
+    double ri = rv[u];
+    if (!entry) ri = __dsub_rn(ri, __dmul_rn(alpha, av[u]));     // krylov.py:307
+    const double zi = dinv ? __dmul_rn(ri, dv[u]) : ri;          // preconditioners.py:61
+    zs[i] = zi;
+    if (lead) {
       if (!entry) {
-        // krylov.py:306-307  x = x + alpha * p ; r = r - alpha * Ap
-        x[i] = __dadd_rn(xv[u], __dmul_rn(alpha, pv[u]));
-        ri = __dsub_rn(ri, __dmul_rn(alpha, av[u]));
-        r[i] = ri;
+        x[i] = __dadd_rn(xv[u], __dmul_rn(alpha, pv[u]));          // krylov.py:306
+        rout[i] = ri;
       }
-      // preconditioners.py:61  r * inv_diag  (identity: r.copy())
-      const double zi = dinv ? __dmul_rn(ri, dv[u]) : ri;
       z[i] = zi;
-      zr[u] = zi;
       acc[0] = fma(ri, ri, acc[0]);
       acc[1] = fma(ri, zi, acc[1]);
     }
-    // K4: this chunk's share of c = cross' z, kColGroup columns at a time; each
-    // thread multiplies its own rows by its own z (no barrier needed), then the
-    // group is reduced across the block in a fixed order.
-    for (int64_t j0 = 0; j0 < m; j0 += kColGroup) {
-      double a[kColGroup];
+  }
+  double* part = P.partials;
+  if (lead) {
+    block_sum<2>(acc, scratch);  // includes the barrier that publishes zs
+    if (threadIdx.x == 0) {
+      part[0 * nchunks + chunk] = acc[0];
+      part[1 * nchunks + chunk] = acc[1];
+    }
+  } else {
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool vec = ((P.ldc & 1) == 0) && ((((uintptr_t)P.cross) | (beg * 8)) & 15) == 0;
+#pragma unroll 1
+  for (int c = 0; c < kProjCols / 8; ++c) {
+    const int64_t j = (int64_t)blockIdx.y * kProjCols + c * 8 + warp;
+    if (j >= m) break;
+    const double* __restrict__ col = P.cross + j * P.ldc + beg;
+    double a = 0.0;
+    if (vec && rows == kProjChunk) {
+      double2 cv[kProjChunk / 64];
 #pragma unroll
-      for (int c = 0; c < kColGroup; ++c) a[c] = 0.0;
+      for (int t = 0; t < kProjChunk / 64; ++t) cv[t] = __ldcs(reinterpret_cast<const double2*>(col) + t * 32 + lane);
 #pragma unroll
-      for (int u = 0; u < kRows; ++u) {
-        const int64_t i = i0 + (int64_t)u * kUpdThreads;
-        if (i < n) {
-#pragma unroll
-          for (int c = 0; c < kColGroup; ++c)
-            if (j0 + c < m) a[c] = fma(__ldcs(cross + (j0 + c) * P.ldc + i), zr[u], a[c]);
-        }
+      for (int t = 0; t < kProjChunk / 64; ++t) {
+        const double2 zz = reinterpret_cast<const double2*>(zs)[t * 32 + lane];
+        a = fma(cv[t].x, zz.x, a);
+        a = fma(cv[t].y, zz.y, a);
       }
-#pragma unroll
-      for (int c = 0; c < kColGroup; ++c) a[c] = warp_sum(a[c]);
-      if (lane == 0) {
-#pragma unroll
-        for (int c = 0; c < kColGroup; ++c) wsum[warp * kColGroup + c] = a[c];
-      }
-      __syncthreads();
-      if (threadIdx.x < kColGroup && j0 + threadIdx.x < m) {
-        double t = 0.0;
-#pragma unroll
-        for (int w = 0; w < kUpdThreads / 32; ++w) t += wsum[w * kColGroup + threadIdx.x];
-        red[2 + j0 + threadIdx.x] += t;
-      }
-      __syncthreads();
+    } else {
+      for (int i = lane; i < rows; i += 32) a = fma(__ldcs(col + i), zs[i], a);
+    }
+    a = warp_sum(a);
+    if (lane == 0) part[(2 + j) * nchunks + chunk] = a;
+  }
+}
+
+// Combine the update partials (one warp per value, fixed order) and, in the
+// last block to finish, record ||r||, test convergence, form beta and solve mu.
+__global__ void __launch_bounds__(256) k_pcg_finish(const rk_pcg_plan P, int entry, int64_t nchunks) {
+  rk_pcg_state* st = P.st;
+  if (st->done) return;
+  extern __shared__ double dyn[];      // red[2 + m] | ysm[2 w] | Ls[w*w]
+  const int64_t m = P.m;
+  const int64_t nv = 2 + m;
+  const double* part = P.partials;
+  double* sums = P.partials + nv * nchunks;
+  const int lane = threadIdx.x & 31;
+  const int64_t v = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (v < nv) {
+    const double* pv = part + v * nchunks;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;  // 4 independent chains, fixed order
+    int64_t b = lane;
+    for (; b + 96 < nchunks; b += 128) {
+      a0 += __ldcg(pv + b);
+      a1 += __ldcg(pv + b + 32);
+      a2 += __ldcg(pv + b + 64);
+      a3 += __ldcg(pv + b + 96);
+    }
+    for (; b < nchunks; b += 32) a0 += __ldcg(pv + b);
+    double a = warp_sum((a0 + a1) + (a2 + a3));
+    if (lane == 0) {
+      sums[v] = a;
+      __threadfence();  // publish before the block's ticket
     }
   }
-  block_sum<2>(acc, scratch);
-  if (threadIdx.x == 0) { red[0] = acc[0]; red[1] = acc[1]; }
+  if (!ticket_last(P.tickets + 1)) return;
+  __threadfence();
+  double* red = dyn;
+  for (int64_t j = threadIdx.x; j < nv; j += blockDim.x) red[j] = __ldcg(sums + j);
   __syncthreads();
-  const int nv = (int)(2 + m);
-  if (!publish_and_check_last(red, nv, P.partials, P.tickets + 1)) return;
-
-  // ---- last block: combine, record, decide, solve --------------------------
-  combine_partials(P.partials, gridDim.x, nv, red);
+  const int64_t k = st->k;
   __shared__ int s_stop;
   if (threadIdx.x == 0) {
     const double rr = red[0], rz_next = red[1];
@@ -313,7 +246,7 @@ __global__ void __launch_bounds__(kUpdThreads) k_pcg_update(const rk_pcg_plan P,
   }
   __syncthreads();
   if (s_stop || m == 0) return;
-  double* ysm = red + nv;  // 2*wchol scratch
+  double* ysm = red + nv;
   solve_factor(P, red + 2, ysm, ysm + 2 * P.wchol, P.mu);
 }
 
@@ -374,33 +307,18 @@ namespace rkh {
 
 void prof_mark(int slot, cudaStream_t s);
 
-struct UpdGeom {
-  int grid;
-  size_t smem;
-};
+static int64_t update_chunks(int64_t n) { return std::max<int64_t>(1, (n + rk::kProjChunk - 1) / rk::kProjChunk); }
 
-static UpdGeom update_geometry(int64_t n, int64_t m, int64_t wchol) {
-  UpdGeom g;
-  const int64_t nchunks = (n + rk::kUpdChunk - 1) / rk::kUpdChunk;
-  g.smem = (size_t)(2 + m + 2 * wchol + (wchol <= rk::kMaxStagedChol ? wchol * wchol : 0)) * sizeof(double);
-  // one resident wave; chunks are grid-strided so every block does equal work
-  static int occ = [] {
-    int o = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, rk::k_pcg_update, rk::kUpdThreads, 1024) != cudaSuccess ||
-        o < 1)
-      o = 1;
-    return o;
-  }();
-  g.grid = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, (int64_t)occ * sm_count()));
-  return g;
+static size_t finish_smem(int64_t m, int64_t wchol) {
+  return (size_t)(2 + m + 2 * wchol + (wchol <= rk::kMaxStagedChol ? wchol * wchol : 0)) * sizeof(double);
 }
 
 int64_t pcg_workspace_doubles(int64_t n, int64_t m, int64_t vcap) {
   int64_t need = 0;
   // spmv / curvature partials: grid x 2
   need = std::max<int64_t>(need, (int64_t)sm_count() * 8 * 2);
-  // update partials: grid x (2 + m)
-  need = std::max<int64_t>(need, (int64_t)update_geometry(n, m, 0).grid * (2 + m));
+  // update partials (2 + m) x chunks, plus the (2 + m) sums
+  need = std::max<int64_t>(need, (2 + m) * (update_chunks(n) + 1));
   // fom gemv-t partials: chunks x vcap
   need = std::max<int64_t>(need, gemv_nchunks(n) * std::max<int64_t>(vcap, 1));
   return need;
@@ -409,7 +327,7 @@ int64_t pcg_workspace_doubles(int64_t n, int64_t m, int64_t vcap) {
 static int configure_once() {
   static int done = 0;
   if (!done) {
-    cudaFuncSetAttribute(rk::k_pcg_update, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(rk::k_pcg_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(rk::k_pcg_direction, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     done = 1;
   }
@@ -419,7 +337,7 @@ static int configure_once() {
 // need_proj: the kernels that reduce cross'z and solve with the factor (entry,
 // update) need cross/L/sqd; the direction kernel only reads B and mu.
 static int check_plan(const rk_pcg_plan& P, bool need_proj) {
-  RK_REQUIRE(P.st && P.x && P.r && P.z && P.V && P.AV, RK_ERR_ARG, "pcg plan: null vector pointer");
+  RK_REQUIRE(P.st && P.x && P.r && P.r2 && P.z && P.V && P.AV, RK_ERR_ARG, "pcg plan: null vector pointer");
   RK_REQUIRE(P.m >= 0 && P.m <= rk::kMaxProj, RK_ERR_DIMENSION, "pcg plan: projection width %lld unsupported",
              (long long)P.m);
   RK_REQUIRE(P.m == 0 || (P.B && P.mu), RK_ERR_ARG, "pcg plan: projection pointers missing");
@@ -437,8 +355,13 @@ static int check_plan(const rk_pcg_plan& P, bool need_proj) {
 }
 
 static void launch_update(const rk_pcg_plan& P, int entry, cudaStream_t s) {
-  const UpdGeom g = update_geometry(P.n, P.m, P.wchol);
-  rk::k_pcg_update<<<g.grid, rk::kUpdThreads, g.smem, s>>>(P, entry); rkh::note_launch();
+  const int64_t nch = update_chunks(P.n);
+  const int64_t groups = std::max<int64_t>(1, (P.m + rk::kProjCols - 1) / rk::kProjCols);
+  dim3 grid((unsigned)nch, (unsigned)groups);
+  rk::k_pcg_update<<<grid, rk::kUpdThreads, 0, s>>>(P, entry); rkh::note_launch();
+  const int64_t nv = 2 + P.m;
+  const unsigned fgrid = (unsigned)((nv + 7) / 8);
+  rk::k_pcg_finish<<<fgrid, 256, finish_smem(P.m, P.wchol), s>>>(P, entry, nch); rkh::note_launch();
 }
 
 static void launch_direction(const rk_pcg_plan& P, int entry, int64_t kmax, cudaStream_t s) {

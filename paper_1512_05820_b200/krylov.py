@@ -186,7 +186,7 @@ class BlockDiagFactor:
             if kinds and kinds[0] == "chol":
                 L = self._blocks[0][1]
                 w = L.m
-                Ld = L.device(device)
+                Ld = L.device_inverse(device)
                 rest = [b for _, b in self._blocks[1:]]
             else:
                 w, Ld = 0, None
@@ -205,7 +205,8 @@ class BlockDiagFactor:
                     m = block.shape[0]
                     Lfull[np.arange(at, at + m), np.arange(at, at + m)] = block
                     at += m
-            out = (as_block(Lfull, device), self.size, None)
+            Linv = DenseLowerTriangular.from_full(Lfull).device_inverse(device)
+            out = (Linv, self.size, None)
         self._dev[key] = out
         return out
 
@@ -269,6 +270,7 @@ class _Run:
         self.n, self.device, self.mode_code, self.keep_av, self.m = n, device, mode_code, keep_av, m
         self.x = torch.zeros(n, dtype=F64, device=device)
         self.r = torch.empty(n, dtype=F64, device=device)
+        self.r2 = torch.empty(n, dtype=F64, device=device)  # residual ping-pong buffer
         self.z = torch.empty(n, dtype=F64, device=device)
         self.mu = torch.zeros(max(m, 1), dtype=F64, device=device)
         self.st = torch.zeros(nat.STATE_BYTES, dtype=torch.uint8, device=device)
@@ -308,7 +310,7 @@ class _Run:
     def _fill_plan(self):
         P = self.plan
         P.n = self.n
-        P.x, P.r, P.z = self.x.data_ptr(), self.r.data_ptr(), self.z.data_ptr()
+        P.x, P.r, P.r2, P.z = self.x.data_ptr(), self.r.data_ptr(), self.r2.data_ptr(), self.z.data_ptr()
         P.V, P.ldv, P.vcap = self.V.data_ptr(), block_ld(self.V), self.vcap
         if self.keep_av:
             P.AV, P.ldav = self.AV.data_ptr(), block_ld(self.AV)

@@ -615,9 +615,21 @@ class DenseLowerTriangular:
             t = self._dev[key] = as_block(self._full, device)
         return t
 
+    def device_inverse(self, device) -> torch.Tensor:
+        """Column-major device copy of L^{-1} (LAPACK dtrtri): the fused PCG
+        kernels apply F^{-1} = L^{-T} L^{-1} as two triangular mat-vecs."""
+        key = ("inv", device.type, device.index)
+        t = self._dev.get(key)
+        if t is None:
+            Linv, info = scipy.linalg.lapack.dtrtri(self._full, lower=1)
+            if info != 0:
+                raise NotPositiveDefinite("singular Cholesky factor", pivot=int(info - 1) if info > 0 else None)
+            t = self._dev[key] = as_block(np.tril(Linv), device)
+        return t
+
     def device_form(self, device):
-        """(L, w, sqd=None) in the form the fused PCG kernels take."""
-        return (self.device(device) if self.m else None, self.m, None)
+        """(Linv, w, sqd=None) in the form the fused PCG kernels take."""
+        return (self.device_inverse(device) if self.m else None, self.m, None)
 
     def solve_lower(self, rhs):
         return scipy.linalg.solve_triangular(self._full, np.asarray(rhs, dtype=np.float64), lower=True)
