@@ -205,6 +205,9 @@ def run_b200(args, rank, world, dist):
         pk.run_sequence(dseq, cfg, precond_factory=jac)
     torch.cuda.synchronize()
 
+    from paper_1512_05820_b200 import _timing
+
+    _timing.reset()
     stream = torch.cuda.current_stream()
     times = []
     reports = None
@@ -294,6 +297,8 @@ def run_b200(args, rank, world, dist):
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
     }
+    if _timing.ENABLED:  # diagnostic only: adds synchronisations, never on the reported line by default
+        line["phases_s_per_step"] = {k: round(v / max(args.steps, 1), 4) for k, v in _timing.TIMES.items()}
     if rank == 0:
         os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
         with open(os.path.join(ROOT, "gpurun_out", "c3_schedule.json"), "w") as fh:

@@ -191,6 +191,17 @@ int rk_gram_upper(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m
 int rk_gemm_nn(int64_t n, int64_t s, int64_t y, const double* S, int64_t lds,
                const double* C, int64_t ldc, double* Out, int64_t ldo, void* stream);
 
+/* ---- POD reduced problem on the device (pod.py:86-97,123-131) -------------- */
+/* out = 1/2 (W + W'), W_ab = (gamma_a G_ab) gamma_b. mode 0: full G. mode 1: only
+ * the upper triangle of G is defined (rk_gram_upper output); its column b is
+ * first multiplied by col_scale[b] (NULL = 1) and the triangle mirrored. */
+int rk_pod_weighted_gram(int64_t m, const double* G, int64_t ldg, int32_t mode, const double* col_scale,
+                         const double* gamma, double* out, int64_t ldo, void* stream);
+/* coef[:, j] = V[:, m-1-j] / sigma[j] * gamma for j < y (V: eigenvectors of the
+ * weighted Gram in ascending eigenvalue order, as LAPACK/cuSOLVER return them). */
+int rk_pod_coef(int64_t m, int64_t y, const double* V, int64_t ldv, const double* sigma,
+                const double* gamma, double* coef, int64_t ldc, void* stream);
+
 /* ---- measurement hooks (bench.py only; not thread-safe) --------------------
  * Between begin and end, rk_pcg_steps brackets each of its three kernels
  * (0: K1 SpMV+curvature, 1: K3/K4 update+projection, 2: K5 direction) with

@@ -121,6 +121,8 @@ _SIGNATURES = {
     "rk_gram_upper": (c_i32, [c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64,
                               c_vp]),
     "rk_gemm_nn": (c_i32, [c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp]),
+    "rk_pod_weighted_gram": (c_i32, [c_i64, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "rk_pod_coef": (c_i32, [c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "rk_profile_begin": (c_i32, []),
     "rk_launch_count": (c_i64, []),
     "rk_profile_end": (c_i32, [ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64)]),

@@ -60,6 +60,11 @@ static ProfState g_prof;
 static std::atomic<int64_t> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+bool prof_sample() {
+  static uint64_t counter = 0;
+  return g_prof.on && ((counter++ & 7u) == 0);
+}
+
 void prof_mark(int slot, cudaStream_t s) {
   if (!g_prof.on) return;
   if (g_prof.used == g_prof.pool.size()) {

@@ -414,14 +414,41 @@ def gram(X: torch.Tensor, Y: torch.Tensor) -> torch.Tensor:
     return G
 
 
-def symmetric_gram_from_products(Z: torch.Tensor, products, col_scale=None) -> np.ndarray:
-    """Host copy of the symmetric Z'AZ from cached products A Z.
+class UpperGram:
+    """Symmetric Gram Z'AZ kept on the device as its upper triangle.
+
+    ``store`` is an (m, m) tensor read as a column-major matrix (ld = m) whose
+    upper 64x64 tiles were produced by rk_gram_upper; ``scale`` (device vector
+    or None) multiplies column b of the triangle. ``np.asarray`` gives the full
+    mirrored host matrix (the reference's ``gram_zz``)."""
+
+    def __init__(self, store: torch.Tensor, scale: torch.Tensor | None):
+        self.store = store
+        self.scale = scale
+        self.m = int(store.shape[0])
+
+    def __array__(self, dtype=None, copy=None):
+        G = self.store.cpu().numpy().T.copy()  # G[a, b], a row, b column
+        if self.scale is not None:
+            G = G * self.scale.cpu().numpy()[None, :]
+        iu = np.triu_indices(self.m, 1)
+        G[(iu[1], iu[0])] = G[iu]
+        return G if dtype is None else G.astype(dtype)
+
+    @property
+    def shape(self):
+        return (self.m, self.m)
+
+
+def symmetric_gram_from_products(Z: torch.Tensor, products, col_scale=None) -> UpperGram:
+    """Z'AZ from cached products A Z (no SpMM).
 
     ``products`` is a list of (AZ_block, col_off): AZ_block holds A applied to
-    columns [col_off, col_off + w) of Z (e.g. the stage-1 product A W and the
-    stored A p_k of the PCG run). Only the upper 64x64 tiles are computed on the
-    device (rk_gram_upper) and mirrored here; ``col_scale`` (length m or None)
-    rescales column j afterwards (products of unscaled directions)."""
+    columns [col_off, col_off + w) of Z (the stage-1 product A W and the stored
+    A p_k of the PCG run). Only the upper 64x64 tiles are computed
+    (rk_gram_upper, half the flops of the reference's full B'(AB));
+    ``col_scale`` (length m or None) rescales column j (products of unscaled
+    directions)."""
     n, m = Z.shape
     dev = Z.device
     store = torch.zeros((max(m, 1), max(m, 1)), dtype=F64, device=dev)  # column-major m x m (ld = m)
@@ -435,12 +462,8 @@ def symmetric_gram_from_products(Z: torch.Tensor, products, col_scale=None) -> n
         nat.check(nat.lib().rk_gram_upper(n, m, Z.data_ptr(), block_ld(Z), w, AB.data_ptr(), block_ld(AB), off,
                                           Gblk.data_ptr(), m, ws.data_ptr(), ws.numel(), nat.stream_ptr(dev)),
                   "gram_upper")
-    G = store[:m, :m].cpu().numpy().T.copy()  # G[a, b] with a row, b column
-    if col_scale is not None:
-        G = G * np.asarray(col_scale, dtype=np.float64)[None, :]
-    iu = np.triu_indices(m, 1)
-    G[(iu[1], iu[0])] = G[iu]
-    return G
+    scale = as_vector(col_scale, dev) if col_scale is not None else None
+    return UpperGram(store[:m, :m], scale)
 
 
 def gemm_nn(S: torch.Tensor, C, out: torch.Tensor | None = None) -> torch.Tensor:

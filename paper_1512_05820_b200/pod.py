@@ -8,14 +8,28 @@ spectrum and the energy truncation agree with the oracle to Gram rounding.
 
 from __future__ import annotations
 
+import os
 import warnings
 from dataclasses import dataclass
 
 import numpy as np
 import torch
 
+from . import _native as nat
+from ._timing import phase as _phase
 from .errors import DimensionMismatch, EmptyBasis, RankTruncatedWarning
-from .linalg import DenseBasis, SparseSpdMatrix, as_block, as_matrix, assemble_gram, gemm_nn, symmetric_evd, to_numpy
+from .linalg import (
+    DenseBasis,
+    SparseSpdMatrix,
+    UpperGram,
+    as_block,
+    as_matrix,
+    assemble_gram,
+    block_ld,
+    gemm_nn,
+    symmetric_evd,
+    to_numpy,
+)
 
 _RANK_RTOL = 1e-12  # pod.py:30, on sigma^2 relative to the largest
 
@@ -87,15 +101,66 @@ def _finalize(S, gamma, sigma, V, eps, max_cols=None):
     )
 
 
+DEVICE_EVD_MIN = int(os.environ.get("RK_DEVICE_EVD_MIN", "128"))
+
+
 def pod_evd_from_gram(gram_sts, S, gamma, eps: float, *, max_cols: int | None = None) -> PodBasisResult:
-    """Method of snapshots from a precomputed S'Theta S (pod.py:123-131)."""
+    """Method of snapshots from a precomputed S'Theta S (pod.py:123-131).
+
+    For m >= DEVICE_EVD_MIN (default 128) the reduced problem stays on the
+    device: weighted Gram (rk_pod_weighted_gram), cuSOLVER syevd
+    (torch.linalg.eigh, the K9 "small on-device eigensolver"), coefficients
+    (rk_pod_coef); only the m eigenvalues come to the host for the energy
+    criterion. Smaller problems use host LAPACK dsyevd exactly as the reference."""
     Sd = as_block(S)
     gamma = np.asarray(to_numpy(gamma), dtype=np.float64)
-    G = np.asarray(to_numpy(gram_sts), dtype=np.float64)
+    m = gamma.shape[0]
+    if m >= DEVICE_EVD_MIN and isinstance(Sd, torch.Tensor):
+        return _pod_device(gram_sts, Sd, gamma, eps, max_cols)
+    G = np.asarray(gram_sts, dtype=np.float64) if isinstance(gram_sts, UpperGram) else \
+        np.asarray(to_numpy(gram_sts), dtype=np.float64)
     weighted = gamma[:, None] * G * gamma[None, :]
-    eigs, V = symmetric_evd(0.5 * (weighted + weighted.T))
+    with _phase("trunc_evd"):
+        eigs, V = symmetric_evd(0.5 * (weighted + weighted.T))
     sigma = np.sqrt(np.maximum(eigs, 0.0))
     return _finalize(Sd, gamma, sigma, V, eps, max_cols=max_cols)
+
+
+def _pod_device(gram_sts, Sd, gamma, eps, max_cols):
+    dev = Sd.device
+    m = gamma.shape[0]
+    st = nat.stream_ptr(dev)
+    gam_d = torch.from_numpy(np.ascontiguousarray(gamma)).to(dev)
+    if isinstance(gram_sts, UpperGram):
+        G, mode, scale = gram_sts.store, 1, gram_sts.scale
+        ldg = m
+    else:
+        G = as_block(gram_sts, dev)
+        mode, scale, ldg = 0, None, block_ld(G)
+    Wt = torch.empty((m, m), dtype=torch.float64, device=dev)  # symmetric: layout-agnostic
+    nat.check(nat.lib().rk_pod_weighted_gram(m, G.data_ptr(), ldg, mode, scale.data_ptr() if scale is not None
+                                             else None, gam_d.data_ptr(), Wt.data_ptr(), m, st), "pod weighted gram")
+    with _phase("trunc_evd"):
+        evals, evecs = torch.linalg.eigh(Wt)  # ascending, like LAPACK
+        eigs = evals.cpu().numpy()[::-1].copy()
+    if np.all(gamma == 0.0):
+        raise EmptyBasis("all snapshot weights are zero")
+    sigma = np.sqrt(np.maximum(eigs, 0.0))
+    y = energy_truncation_dim(np.maximum(sigma, 0.0) ** 2, eps)
+    ncols = y if max_cols is None else min(y, int(max_cols))
+    Vcm = evecs.t().contiguous()  # row i = eigenvector i -> column-major V with ld = m
+    coef = torch.empty((max(ncols, 1), m), dtype=torch.float64, device=dev)  # column-major m x ncols
+    sig_d = torch.from_numpy(np.ascontiguousarray(sigma[:ncols])).to(dev)
+    nat.check(nat.lib().rk_pod_coef(m, ncols, Vcm.data_ptr(), m, sig_d.data_ptr(), gam_d.data_ptr(),
+                                    coef.data_ptr(), m, st), "pod coef")
+    coef_cm = coef[:ncols].t()  # (m, ncols) view, column-major
+    cols = gemm_nn(Sd, coef_cm)
+    return PodBasisResult(
+        basis=DenseBasis(cols, gram_diag=np.ones(ncols)),
+        singular_values=np.maximum(sigma, 0.0),
+        y=y,
+        snapshot_coef=coef_cm.cpu().numpy(),
+    )
 
 
 def pod_evd(S, gamma, theta, eps: float, *, max_cols: int | None = None) -> PodBasisResult:

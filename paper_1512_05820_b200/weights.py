@@ -58,7 +58,8 @@ class WeightHistory:
 
     def reexpress(self, trunc_map, gram) -> None:
         """Project every entry onto the post-truncation basis: map' gram eta."""
-        proj = np.asarray(trunc_map).T @ np.asarray(gram)
+        g = gram.detach().cpu().numpy() if hasattr(gram, "detach") else np.asarray(gram)
+        proj = np.asarray(trunc_map).T @ g
         self._entries = [proj @ self.padded(i) for i in range(len(self._entries))]
 
 
