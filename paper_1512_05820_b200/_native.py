@@ -36,6 +36,10 @@ class RkCsr(ctypes.Structure):
         ("val", c_vp),
         ("lanes", c_i32),
         ("pad_", c_i32),
+        ("nblk", c_i64),
+        ("browptr", c_vp),
+        ("bcol", c_vp),
+        ("bval", c_vp),
     ]
 
 
@@ -111,6 +115,7 @@ _SIGNATURES = {
     "rk_spmm": (c_i32, [ctypes.POINTER(RkCsr), c_i64, c_vp, c_i64, c_vp, c_i64, c_vp]),
     "rk_csr_diagonal": (c_i32, [ctypes.POINTER(RkCsr), c_vp, c_vp, c_vp, c_vp]),
     "rk_csr_asymmetry": (c_i32, [ctypes.POINTER(RkCsr), c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "rk_bsr3_gather": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp]),
     "rk_gemv_t": (c_i32, [c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "rk_gemv_n": (c_i32, [c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_i32, c_vp]),
     "rk_dot": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),

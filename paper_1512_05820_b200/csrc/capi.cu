@@ -116,8 +116,12 @@ static int check_csr(const rk_csr* A) {
   RK_REQUIRE(A->lanes == 0 || A->lanes == 1 || A->lanes == 2 || A->lanes == 4 || A->lanes == 8 ||
                  A->lanes == 16 || A->lanes == 32,
              RK_ERR_ARG, "CSR: lanes must be 0 or a power of two <= 32");
+  RK_REQUIRE(!A->bval || (A->browptr && A->bcol && A->n % 3 == 0 && A->nblk * 9 == A->nnz), RK_ERR_ARG,
+             "CSR: inconsistent 3x3 block view");
   return RK_OK;
 }
+
+int launch_bsr3_gather(int64_t nblk, const int32_t* perm, const double* val, double* bval, cudaStream_t s);
 
 }  // namespace rkh
 
@@ -189,6 +193,12 @@ int rk_csr_diagonal(const rk_csr* A, double* diag, double* dinv, int64_t* bad_ro
   if (int e = rkh::check_csr(A)) return e;
   RK_REQUIRE(bad_row, RK_ERR_ARG, "rk_csr_diagonal: null bad_row");
   return rkh::launch_csr_diagonal(*A, diag, dinv, bad_row, as_stream(stream));
+}
+
+int rk_bsr3_gather(int64_t nblk, const int32_t* perm, const double* val, double* bval, void* stream) {
+  RK_REQUIRE(nblk >= 0, RK_ERR_DIMENSION, "rk_bsr3_gather: bad size");
+  RK_REQUIRE(nblk == 0 || (perm && val && bval), RK_ERR_ARG, "rk_bsr3_gather: null pointer");
+  return rkh::launch_bsr3_gather(nblk, perm, val, bval, as_stream(stream));
 }
 
 int rk_csr_asymmetry(const rk_csr* A, double* out2, double* ws, int64_t ws_len, uint32_t* tickets, void* stream) {

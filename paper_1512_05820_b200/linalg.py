@@ -18,6 +18,7 @@ reduced problems bit-compatible with the oracle; everything of size N runs in
 
 from __future__ import annotations
 
+import os
 import threading
 from dataclasses import dataclass
 
@@ -171,28 +172,79 @@ def hstack_blocks(blocks, n: int, device, cap_extra: int = 0) -> torch.Tensor:
 # CSR matrix
 # ---------------------------------------------------------------------------
 _pattern_cache_lock = threading.Lock()
-_pattern_cache: list = []  # [(host rowptr, host col, device rowptr, device col)]
+_pattern_cache: list = []  # [(host rowptr, host col, _Pattern)]
+USE_BSR3 = os.environ.get("RK_BSR", "1") != "0"
+
+
+class _Bsr3:
+    """3x3 block view of a CSR pattern: block row pointers, block columns and
+    the permutation that gathers CSR values into structure-of-arrays blocks."""
+
+    def __init__(self, browptr, bcol, perm, nblk):
+        self.browptr, self.bcol, self.perm, self.nblk = browptr, bcol, perm, int(nblk)
+
+
+class _Pattern:
+    def __init__(self, rowptr: torch.Tensor, col: torch.Tensor, bsr: _Bsr3 | None):
+        self.rowptr, self.col, self.bsr = rowptr, col, bsr
+
+
+def _bsr3_from_host(rp: np.ndarray, ci: np.ndarray, n: int, device) -> _Bsr3 | None:
+    """Detect an exact 3x3 block structure (rows 3i..3i+2 share block columns,
+    columns come in aligned triples) and build its device view; None if not."""
+    if n == 0 or n % 3 or ci.size == 0 or ci.size % 9:
+        return None
+    rp = np.asarray(rp, dtype=np.int64)
+    lens = np.diff(rp)
+    if np.any(lens % 3):
+        return None
+    lr = lens.reshape(-1, 3)
+    if not (np.array_equal(lr[:, 0], lr[:, 1]) and np.array_equal(lr[:, 0], lr[:, 2])):
+        return None
+    t = np.asarray(ci, dtype=np.int64).reshape(-1, 3)
+    if not (np.all(t[:, 0] % 3 == 0) and np.all(t[:, 1] == t[:, 0] + 1) and np.all(t[:, 2] == t[:, 0] + 2)):
+        return None
+    nbr = n // 3
+    nb_per = lr[:, 0] // 3
+    browptr = np.zeros(nbr + 1, dtype=np.int64)
+    np.cumsum(nb_per, out=browptr[1:])
+    nblk = int(browptr[-1])
+    b_row = np.repeat(np.arange(nbr, dtype=np.int64), nb_per)
+    t_loc = np.arange(nblk, dtype=np.int64) - browptr[b_row]
+    first = [rp[3 * b_row + a] for a in range(3)]            # CSR start of rows 3i+a
+    bcol = t[first[0] // 3 + t_loc, 0] // 3
+    for a in (1, 2):
+        if not np.array_equal(t[first[a] // 3 + t_loc, 0] // 3, bcol):
+            return None
+    perm = np.empty(9 * nblk, dtype=np.int64)
+    for a in range(3):
+        for c in range(3):
+            perm[(3 * a + c) * nblk : (3 * a + c + 1) * nblk] = first[a] + 3 * t_loc + c
+    to = lambda arr: torch.from_numpy(np.ascontiguousarray(arr, dtype=np.int32)).to(device)  # noqa: E731
+    return _Bsr3(to(browptr), to(bcol), to(perm), nblk)
 
 
 def _pattern_known(rowptr: np.ndarray, col: np.ndarray, device) -> bool:
     """Same host pattern objects already uploaded (and checked) for this device."""
     with _pattern_cache_lock:
-        return any(dr.device == device and hr is rowptr and hc is col for hr, hc, dr, dc in _pattern_cache)
+        return any(p.rowptr.device == device and hr is rowptr and hc is col for hr, hc, p in _pattern_cache)
 
 
-def _device_pattern(rowptr: np.ndarray, col: np.ndarray, device):
+def _device_pattern(rowptr: np.ndarray, col: np.ndarray, device, n: int) -> _Pattern:
     with _pattern_cache_lock:
-        for hr, hc, dr, dc in _pattern_cache:
-            if dr.device == device and (hr is rowptr or np.array_equal(hr, rowptr)) and (
+        for hr, hc, p in _pattern_cache:
+            if p.rowptr.device == device and (hr is rowptr or np.array_equal(hr, rowptr)) and (
                 hc is col or (hc.shape == col.shape and np.array_equal(hc, col))
             ):
-                return dr, dc
+                return p
     dr = torch.from_numpy(np.ascontiguousarray(rowptr, dtype=np.int32)).to(device)
     dc = torch.from_numpy(np.ascontiguousarray(col, dtype=np.int32)).to(device)
+    bsr = _bsr3_from_host(rowptr, col, n, device) if USE_BSR3 else None
+    p = _Pattern(dr, dc, bsr)
     with _pattern_cache_lock:
-        _pattern_cache.insert(0, (rowptr, col, dr, dc))
+        _pattern_cache.insert(0, (rowptr, col, p))
         del _pattern_cache[2:]
-    return dr, dc
+    return p
 
 
 class SparseSpdMatrix:
@@ -206,17 +258,20 @@ class SparseSpdMatrix:
     """
 
     def __init__(self, n, row_offsets, col_indices, values, *, device=None, validate: bool = True,
-                 lanes: int = 0):
+                 lanes: int = 0, _pattern: "_Pattern | None" = None):
         self.n = int(n)
         dev = device if device is not None else nat.require_device()
         self.device = torch.device(dev)
-        if isinstance(row_offsets, torch.Tensor) and isinstance(col_indices, torch.Tensor):
+        if _pattern is not None:
+            pattern = _pattern
+        elif isinstance(row_offsets, torch.Tensor) and isinstance(col_indices, torch.Tensor):
             rp = row_offsets.to(self.device, torch.int32).contiguous()
             ci = col_indices.to(self.device, torch.int32).contiguous()
             if rp.shape != (self.n + 1,):
                 raise DimensionMismatch(
                     f"row_offsets must have length n+1={self.n + 1}, got {tuple(rp.shape)}"
                 )
+            pattern = _Pattern(rp, ci, None)
         else:
             rp_h = np.asarray(row_offsets)
             ci_h = np.asarray(col_indices)
@@ -232,17 +287,29 @@ class SparseSpdMatrix:
                 rp_h, ci_h, values = csr.indptr, csr.indices, csr.data
             if rp_h.size and int(rp_h[-1]) >= 2**31:
                 raise DimensionMismatch("nnz must be < 2^31 for the int32 device layout")
-            rp, ci = _device_pattern(rp_h, ci_h, self.device)
+            pattern = _device_pattern(rp_h, ci_h, self.device, self.n)
         if isinstance(values, torch.Tensor):
             vals = values.to(self.device, F64).contiguous()
         else:
             vals = torch.from_numpy(np.ascontiguousarray(np.asarray(values, dtype=np.float64))).to(self.device)
+        rp, ci = pattern.rowptr, pattern.col
+        self._pattern = pattern
         self.rowptr = rp
         self.col = ci
         self.values = vals
         self.nnz = int(vals.numel())
         self.lanes = int(lanes)
         self._csr = nat.RkCsr(self.n, self.nnz, rp.data_ptr(), ci.data_ptr(), vals.data_ptr(), self.lanes, 0)
+        self.bval = None
+        bsr = pattern.bsr
+        if bsr is not None and bsr.nblk * 9 == self.nnz:
+            # 3x3 block values for the SpMV kernels (one gather per matrix)
+            self.bval = torch.empty(9 * bsr.nblk, dtype=F64, device=self.device)
+            nat.check(nat.lib().rk_bsr3_gather(bsr.nblk, bsr.perm.data_ptr(), vals.data_ptr(), self.bval.data_ptr(),
+                                               nat.stream_ptr(self.device)), "bsr3 gather")
+            c = self._csr
+            c.nblk, c.browptr, c.bcol, c.bval = bsr.nblk, bsr.browptr.data_ptr(), bsr.bcol.data_ptr(), \
+                self.bval.data_ptr()
         self._diag = None
         self._dinv = None
         self._bad_diag = None
@@ -286,7 +353,7 @@ class SparseSpdMatrix:
     def with_values(self, values, validate: bool = True) -> "SparseSpdMatrix":
         """Same sparsity pattern, new values (per-system refresh of a sequence)."""
         return SparseSpdMatrix(self.n, self.rowptr, self.col, values, device=self.device, validate=validate,
-                               lanes=self.lanes)
+                               lanes=self.lanes, _pattern=self._pattern)
 
     def _validate(self) -> None:
         s = nat.scratch(self.device)

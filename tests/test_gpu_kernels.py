@@ -48,6 +48,25 @@ def test_spmv_all_lane_widths(pk, lanes):
         np.testing.assert_allclose(got, ref, rtol=1e-13, atol=1e-13 * np.abs(ref).max())
 
 
+def test_bsr3_view_for_vector_problems(pk):
+    """Q1 elasticity has exact 3x3 blocks: the SpMV streams the BSR view and
+    matches scipy's CSR product; the fused PCG SpMV agrees with the plain one."""
+    from paper_1512_05820_b200.problems import elasticity_sequence
+
+    H = next(iter(elasticity_sequence((5, 4, 3), p=1))).A
+    A = pk.SparseSpdMatrix(H.n, H.row_offsets, H.col_indices, H.values)
+    assert A.bval is not None and A._pattern.bsr.nblk * 9 == A.nnz
+    x = np.random.default_rng(9).standard_normal(H.n)
+    ref = H.to_scipy() @ x
+    np.testing.assert_allclose(pk.spmv(A, x).cpu().numpy(), ref, rtol=1e-13, atol=1e-13 * np.abs(ref).max())
+    # values refreshed on the same pattern are gathered again
+    A2 = A.with_values(torch.from_numpy(2.0 * H.values).cuda())
+    np.testing.assert_allclose(pk.spmv(A2, x).cpu().numpy(), 2.0 * ref, rtol=1e-13, atol=1e-13 * np.abs(ref).max())
+    # a scalar problem has no block view
+    B = pk.SparseSpdMatrix.from_diagonal(np.arange(1.0, 8.0))
+    assert B.bval is None
+
+
 def test_spmv_sink_counts_one_matvec(pk):
     A = pk.SparseSpdMatrix.identity(5)
     sink = pk.InstrumentationSink()
