@@ -254,6 +254,7 @@ def run_b200(args, rank, world, dist):
         t_e2e = max_over_ranks(time.perf_counter() - t0, dist)
         e2e = {"value": round(t_e2e / world, 4), "unit": UNIT, "h2d_bytes_per_step": int(h2d * world),
                "d2h_bytes_per_step": int(d2h * world),
+               "solve_wall_sum_s": round(sum(r.wall_time for r in reps_e), 3),
                "path": "run_sequence over host CSR (reference-style SparseSpdMatrix fields), solutions copied back"}
         del xh
 

@@ -130,6 +130,22 @@ def as_block(B, device=None) -> torch.Tensor:
     return out
 
 
+_STAGE_MIN_BYTES = 1 << 22
+
+
+def host_to_device(arr: np.ndarray, device, dtype=np.float64) -> torch.Tensor:
+    """H2D copy of a host array. Large arrays are staged through pinned memory
+    with np.copyto (which releases the GIL) and sent with an asynchronous DMA, so
+    a prefetching helper thread does not stall the thread launching kernels; the
+    torch host allocator keeps the pinned block alive until the copy is done."""
+    a = np.ascontiguousarray(np.asarray(arr, dtype=dtype))
+    if a.nbytes < _STAGE_MIN_BYTES:
+        return torch.from_numpy(a).to(device)
+    stage = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, pin_memory=True)
+    np.copyto(stage.numpy(), a)
+    return stage.to(device, non_blocking=True)
+
+
 def as_vector(x, device=None, copy: bool = False) -> torch.Tensor:
     """Contiguous float64 device vector."""
     if device is None:
@@ -140,8 +156,7 @@ def as_vector(x, device=None, copy: bool = False) -> torch.Tensor:
             t = t.reshape(-1)
         t = t.contiguous()
         return t.clone() if copy and t.data_ptr() == x.data_ptr() else t
-    arr = np.ascontiguousarray(np.asarray(x, dtype=np.float64).reshape(-1))
-    return torch.from_numpy(arr).to(device)
+    return host_to_device(np.asarray(x, dtype=np.float64).reshape(-1), device)
 
 
 def to_numpy(t) -> np.ndarray:
@@ -291,7 +306,7 @@ class SparseSpdMatrix:
         if isinstance(values, torch.Tensor):
             vals = values.to(self.device, F64).contiguous()
         else:
-            vals = torch.from_numpy(np.ascontiguousarray(np.asarray(values, dtype=np.float64))).to(self.device)
+            vals = host_to_device(values, self.device)
         rp, ci = pattern.rowptr, pattern.col
         self._pattern = pattern
         self.rowptr = rp
