@@ -70,7 +70,7 @@ def workload_config(args, n=None, nnz=None):
         "preconditioner": "jacobi",
         "rtol": 1e-5,
         "truncation": "pod-a-rbf nu_y=1 nu_w=1 storage_cap=60 max_dim=60",
-        "l2": "inputs larger than L2 (780 MB CSR per SpMV); no flush",
+        "l2": "inputs larger than L2 (552 MB of 3x3-block matrix streamed per SpMV, 20 GB of matrices); no flush",
         "parallelism": "replicas (one independent sequence per GPU)",
     }
 
