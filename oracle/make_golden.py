@@ -182,6 +182,85 @@ def run_elasticity(rk):
     return {"elasticity": d}
 
 
+def _ref_sequence(mine):
+    from recykl.linalg import SparseSpdMatrix
+    from recykl.problems import LinearSystemSpec, SystemSequence
+
+    specs = list(mine)
+    return specs, SystemSequence(n=mine.n, systems=[
+        LinearSystemSpec(A=SparseSpdMatrix(s.A.n, s.A.row_offsets, s.A.col_indices, s.A.values), b=s.b,
+                         xbar=None, tol=s.tol) for s in specs])
+
+
+def run_c2_small(rk):
+    """A 10^3 C2-like variable-coefficient diffusion sequence (drifting matrix)."""
+    from recykl import preconditioners
+    from recykl.threestage import SolverConfig, run_sequence
+    from recykl.truncation import TruncationConfig
+
+    from paper_1512_05820_b200.problems import diffusion3d_sequence
+
+    mine = diffusion3d_sequence(10, p=4, rtol=1e-8, seed=4, corr_len=3.0)
+    specs, seq = _ref_sequence(mine)
+    d = {"n": np.int64(mine.n), "c": mine.C[0], "rowptr": specs[0].A.row_offsets, "col": specs[0].A.col_indices}
+    for j, s in enumerate(specs, start=1):
+        d[f"val{j}"], d[f"b{j}"], d[f"tol{j}"] = s.A.values, s.b, np.float64(s.tol)
+    pf = lambda M: preconditioners.build("jacobi", M)  # noqa: E731
+    for tag, mode in (("cg_", "cg"), ("fom_", "fom")):
+        cfg = SolverConfig(truncation=TruncationConfig(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=12,
+                                                       max_dim=12), mode=mode)
+        xs, reps, _ = run_sequence(seq, cfg, precond_factory=pf)
+        d.update(_pack_run(xs, reps, tag))
+        for j, x in enumerate(xs, start=1):
+            d[f"{tag}q{j}"] = np.float64(mine.C[0] @ x)
+    return {"c2_small": d}
+
+
+def run_c3_mid(rk):
+    """A 10^3-element C3-like Q1 elasticity prefix (N = 3630), CG and FOM."""
+    from recykl import preconditioners
+    from recykl.threestage import SolverConfig, run_sequence
+    from recykl.truncation import TruncationConfig
+
+    from paper_1512_05820_b200.problems import elasticity_sequence
+
+    mine = elasticity_sequence((10, 10, 10), p=3, rtol=1e-6, seed=3)
+    specs, seq = _ref_sequence(mine)
+    d = {"n": np.int64(mine.n), "c": mine.C[0], "rowptr": specs[0].A.row_offsets, "col": specs[0].A.col_indices}
+    for j, s in enumerate(specs, start=1):
+        d[f"val{j}"], d[f"b{j}"], d[f"tol{j}"] = s.A.values, s.b, np.float64(s.tol)
+    pf = lambda M: preconditioners.build("jacobi", M)  # noqa: E731
+    for tag, mode in (("cg_", "cg"), ("fom_", "fom")):
+        cfg = SolverConfig(truncation=TruncationConfig(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=30,
+                                                       max_dim=30), mode=mode)
+        xs, reps, _ = run_sequence(seq, cfg, precond_factory=pf)
+        d.update(_pack_run(xs, reps, tag))
+        for j, x in enumerate(xs, start=1):
+            d[f"{tag}q{j}"] = np.float64(mine.C[0] @ x)
+    return {"c3_mid": d}
+
+
+def run_c5_small(rk):
+    """C5 microbench at reduced size: Laplacian 16x16x32, Gaussian S with 256
+    columns, gamma = 1: assemble_gram + pod_evd_from_gram (nu = 1)."""
+    import warnings
+
+    from recykl.linalg import SparseSpdMatrix, assemble_gram
+    from recykl.pod import pod_evd_from_gram
+
+    from paper_1512_05820_b200.problems import laplacian3d, snapshot_matrix
+
+    L = laplacian3d(16, 16, 32)
+    A = SparseSpdMatrix(L.n, L.row_offsets, L.col_indices, L.values)
+    S = snapshot_matrix(L.n, 256, seed=5)
+    G, _ = assemble_gram(A, S)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        res = pod_evd_from_gram(G, S, np.ones(256), 1.0)
+    return {"c5_small": {"n": np.int64(L.n), "m": np.int64(256), "sigma": res.singular_values,
+                         "y": np.int64(res.y), "basis20": res.columns[:, :20].copy(), "G_diag": np.diag(G).copy()}}
+
+
 def run_kernels(rk):
     """Kernel-level goldens: spmv, assemble_gram, pod_evd_from_gram, augmented_pcg."""
     from recykl.krylov import augmented_pcg
@@ -234,6 +313,9 @@ def main():
     blobs.update(run_kernels(rk))
     blobs.update(run_elasticity(rk))
     blobs.update(run_c1(rk))
+    blobs.update(run_c2_small(rk))
+    blobs.update(run_c3_mid(rk))
+    blobs.update(run_c5_small(rk))
     for name, d in blobs.items():
         path = os.path.join(OUT, f"{name}.npz")
         np.savez_compressed(path, **d)

@@ -43,3 +43,6 @@ def counters(d, prefix):
     keys = ("stage3_iters", "stage2_iters", "stage1_dim", "matvecs", "precond_applies", "final_residual",
             "truncated", "converged")
     return {k: d[f"{prefix}{k}"] for k in keys}
+
+
+pattern_sequence = elasticity_sequence  # same layout: rowptr, col, val{j}, b{j}, tol{j}, c

@@ -174,3 +174,29 @@ def test_unsorted_input_is_canonicalised(pk):
     val = np.array([1.0, 4.0, 3.0, 1.0])
     A = pk.SparseSpdMatrix(2, rowptr, col, val)
     np.testing.assert_allclose(pk.spmv(A, np.array([1.0, 2.0])).cpu().numpy(), [6.0, 7.0])
+
+
+def test_c5_small_pod_matches_reference(pk):
+    """C5 at reduced size (Laplacian 16x16x32, 256 Gaussian snapshots): device
+    Gram + on-device reduced eigenproblem vs the reference's LAPACK result."""
+    import warnings
+
+    from paper_1512_05820_b200.problems import laplacian3d, snapshot_matrix
+
+    d = gio.load("c5_small")
+    L = laplacian3d(16, 16, 32)
+    A = pk.SparseSpdMatrix(L.n, L.row_offsets, L.col_indices, L.values)
+    S = snapshot_matrix(L.n, 256, seed=5)
+    G, _ = pk.assemble_gram(A, S)
+    np.testing.assert_allclose(np.diag(G.cpu().numpy()), d["G_diag"], rtol=1e-12)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        res = pk.pod_evd_from_gram(G, S, np.ones(256), 1.0)
+    assert res.y == int(d["y"])
+    sig = d["sigma"]
+    np.testing.assert_allclose(res.singular_values[:200], sig[:200], rtol=1e-10)
+    got = res.columns[:, :20].cpu().numpy()
+    ref = d["basis20"]
+    for j in range(20):
+        s = np.sign(got[:, j] @ ref[:, j])
+        assert np.linalg.norm(s * got[:, j] - ref[:, j]) <= 1e-8 * np.linalg.norm(ref[:, j])

@@ -134,3 +134,30 @@ def test_oracle_kernels_match_reference():
         res = O.aug_pcg(lambda v: O.matvec(A, v, t), d["b"], d["yhat0"], d["Y"], tol=1e-10, mode=mode, max_iter=400)
         assert res.k == int(d[f"{mode}_k"])
         np.testing.assert_allclose(res.x, d[f"{mode}_x"], rtol=1e-10, atol=1e-12)
+
+
+@pytest.mark.parametrize("name,tag,mode,cap", [("c2_small", "cg_", "cg", 12), ("c2_small", "fom_", "fom", 12),
+                                               ("c3_mid", "cg_", "cg", 30), ("c3_mid", "fom_", "fom", 30)])
+def test_oracle_c2_c3_goldens(name, tag, mode, cap):
+    d = gio.load(name)
+    cfg = O.Config(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=cap, max_dim=cap, mode=mode)
+    xs, reps, _ = O.run_sequence(gio.pattern_sequence(d), cfg, precond="jacobi")
+    _same(d, tag, xs, reps, xtol=1e-9)
+    for j, x in enumerate(xs, start=1):
+        q = float(d[f"{tag}q{j}"])
+        assert abs(d["c"] @ x - q) <= 1e-9 * abs(q)
+
+
+def test_oracle_c5_small_pod():
+    import scipy.sparse
+
+    from paper_1512_05820_b200.problems import laplacian3d, snapshot_matrix
+
+    d = gio.load("c5_small")
+    L = laplacian3d(16, 16, 32)
+    S = snapshot_matrix(L.n, 256, seed=5)
+    G, _ = O.gram_with_product(L.to_scipy(), S, None)
+    np.testing.assert_allclose(np.diag(G), d["G_diag"], rtol=1e-12)
+    basis, sigma, y, _ = O.pod_from_gram(G, S, np.ones(256), 1.0)
+    assert y == int(d["y"])
+    np.testing.assert_allclose(sigma, d["sigma"], rtol=1e-10)
