@@ -262,8 +262,10 @@ def run_b200(args, rank, world, dist):
     peaks = _peaks()
     A0 = dev_specs[0].A
     if A0.bval is not None:
-        fmt = "BSR 3x3 (SoA fp64 values, int32 block columns)"
-        alg_bytes = bsr3_bytes(n, A0._pattern.bsr.nblk)
+        bsr = A0._pattern.bsr
+        fmt = (f"SELL-32 of 3x3 blocks (SoA fp64 values, int32 block columns; {bsr.nblk} slots for "
+               f"{bsr.nreal} blocks, {100.0 * (bsr.nblk - bsr.nreal) / bsr.nblk:.1f}% padding)")
+        alg_bytes = bsr3_bytes(n, bsr.nblk)
     else:
         fmt = "CSR (fp64 values, int32 columns)"
         alg_bytes = spmv_bytes(n, nnz)

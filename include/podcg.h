@@ -51,15 +51,18 @@ typedef struct rk_csr {
   const double* val;     /* nnz */
   int32_t lanes;         /* lanes cooperating on one row: 1,2,4,8,16,32 (0 = auto) */
   int32_t pad_;
-  /* Optional 3x3 block view of the same matrix (vector-valued problems such as
-   * the Q1 elasticity operator): when bval != NULL the SpMV kernels stream
-   * 9 values + 1 block index per block instead of 9 x (value + index), i.e.
-   * 76 instead of 108 bytes per 9 nonzeros. Values are stored structure-of-
-   * arrays: bval[e * nblk + b] is entry e = 3*a + c (row a, column c) of
-   * block b; rk_bsr3_gather fills them from val. */
-  int64_t nblk;
-  const int32_t* browptr; /* n/3 + 1 */
-  const int32_t* bcol;    /* nblk block columns */
+  /* Optional sliced-ELL view of the same matrix in 3x3 blocks (vector-valued
+   * problems such as the Q1 elasticity operator; SELL-32: 32 block rows per
+   * slice, padded to the slice's widest row). When bval != NULL the SpMV
+   * kernels stream 9 values + 1 block index per stored block instead of
+   * 9 x (value + index), i.e. 76 instead of 108 bytes per 9 nonzeros.
+   * Slot (slice s, position t, lane l) = browptr[s] + 32 t + l. Values are
+   * structure-of-arrays: bval[e * nblk + slot] is entry e = 3*a + c (row a,
+   * column c) of the block in that slot (0 for padding); rk_bsr3_gather fills
+   * them from val. */
+  int64_t nblk;           /* number of slots (stored blocks + padding) */
+  const int32_t* browptr; /* ceil(n/96) + 1 slice offsets, in slots */
+  const int32_t* bcol;    /* nblk block columns (padding: a valid column) */
   const double* bval;     /* 9 * nblk */
 } rk_csr;
 
@@ -157,8 +160,9 @@ int rk_spmm(const rk_csr* A, int64_t m, const double* X, int64_t ldx, double* Y,
  * (preconditioners.py:54-58, linalg.py:114-119). */
 int rk_csr_diagonal(const rk_csr* A, double* diag, double* dinv, int64_t* bad_row,
                     void* stream);
-/* bval[s] = val[perm[s]] for s < 9*nblk: refresh the 3x3-block values of a matrix
- * whose pattern (and perm) was built once for the sequence. */
+/* bval[s] = perm[s] >= 0 ? val[perm[s]] : 0 for s < 9*nblk: refresh the
+ * 3x3-block slot values of a matrix whose pattern (and perm) was built once
+ * for the sequence. */
 int rk_bsr3_gather(int64_t nblk, const int32_t* perm, const double* val, double* bval, void* stream);
 /* Largest |A_ij - A_ji| over stored entries and max|A_ij| (device doubles [2]);
  * replaces the scipy transpose difference of SparseSpdMatrix._validate

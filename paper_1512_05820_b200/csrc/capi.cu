@@ -116,7 +116,7 @@ static int check_csr(const rk_csr* A) {
   RK_REQUIRE(A->lanes == 0 || A->lanes == 1 || A->lanes == 2 || A->lanes == 4 || A->lanes == 8 ||
                  A->lanes == 16 || A->lanes == 32,
              RK_ERR_ARG, "CSR: lanes must be 0 or a power of two <= 32");
-  RK_REQUIRE(!A->bval || (A->browptr && A->bcol && A->n % 3 == 0 && A->nblk * 9 == A->nnz), RK_ERR_ARG,
+  RK_REQUIRE(!A->bval || (A->browptr && A->bcol && A->n % 3 == 0 && A->nblk * 9 >= A->nnz), RK_ERR_ARG,
              "CSR: inconsistent 3x3 block view");
   return RK_OK;
 }

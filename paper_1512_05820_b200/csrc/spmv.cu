@@ -269,69 +269,71 @@ __global__ void __launch_bounds__(256) k_csr_asymmetry(int64_t n, const int32_t*
 }
 
 // ---------------------------------------------------------------------------
-// 3x3 block SpMV (BSR, structure-of-arrays values). A warp owns one block row
-// (3 matrix rows); lane l takes blocks beg+l, beg+l+32, ...: it loads the
-// block column and the 9 values (each load coalesced across the warp), then
-// gathers the 3 consecutive x entries of the block column. The three row sums
-// are reduced with xor butterflies. 76 bytes per block instead of the 108 the
-// CSR form streams for the same 9 nonzeros.
+// 3x3-block SpMV in sliced-ELL form (SELL-32 of 3x3 blocks, structure-of-
+// arrays values) for vector-valued problems such as the Q1 elasticity
+// operator. A warp owns a slice of 32 block rows, one block row (3 matrix rows)
+// per lane; slot t of the slice is read by all 32 lanes at once, so every load
+// of the block column and of each of the 9 values is a fully coalesced 128- or
+// 256-byte warp access, and the 3 consecutive x entries of the block column
+// are gathered per lane. 76 bytes per stored block (vs 108 for the same 9
+// nonzeros in CSR); slices are padded only to their widest row.
 // ---------------------------------------------------------------------------
-constexpr int kBsrLanes = 16;  // lanes per block row: 2 block rows per warp
-constexpr int kBsrU = 2;       // blocks per lane per pass (16 x 2 = 32 >= 27 Q1 blocks)
-
-__device__ __forceinline__ void bsr3_row(const rk_csr& A, const double* __restrict__ x, int64_t br, bool valid,
-                                         int sub, double& s0, double& s1, double& s2) {
+__device__ __forceinline__ void sell3_row(const rk_csr& A, const double* __restrict__ x, int64_t slice, int lane,
+                                          double& s0, double& s1, double& s2) {
   s0 = s1 = s2 = 0.0;
-  if (valid) {
-    const int32_t beg = __ldg(A.browptr + br), end = __ldg(A.browptr + br + 1);
-    const int64_t nb = A.nblk;
-    // two blocks per lane per pass (j and j + 16), loads issued before use;
-    // the second block is only touched when it exists (no speculative gathers)
-    for (int32_t j = beg + sub; j < end; j += kBsrLanes * kBsrU) {
-      const int32_t j2 = j + kBsrLanes;
-      const bool two = j2 < end;
-      const int32_t ca = __ldcs(A.bcol + j);
-      double va[9], vb[9];
+  const int32_t base = __ldg(A.browptr + slice);
+  const int32_t width = (__ldg(A.browptr + slice + 1) - base) >> 5;
+  const int64_t ns = A.nblk;
+  const int32_t* __restrict__ col = A.bcol + base + lane;
+  const double* __restrict__ val = A.bval + base + lane;
+  int32_t t = 0;
+  for (; t + 2 <= width; t += 2) {  // two slots in flight per lane
+    const int32_t ca = __ldcs(col + 32 * t), cb = __ldcs(col + 32 * (t + 1));
+    double va[9], vb[9];
 #pragma unroll
-      for (int e = 0; e < 9; ++e) va[e] = __ldcs(A.bval + e * nb + j);
-      int32_t cb = 0;
-      if (two) {
-        cb = __ldcs(A.bcol + j2);
-#pragma unroll
-        for (int e = 0; e < 9; ++e) vb[e] = __ldcs(A.bval + e * nb + j2);
-      }
-      const double* xa = x + 3 * (int64_t)ca;
-      const double a0 = __ldg(xa), a1 = __ldg(xa + 1), a2 = __ldg(xa + 2);
-      s0 = fma(va[0], a0, s0); s0 = fma(va[1], a1, s0); s0 = fma(va[2], a2, s0);
-      s1 = fma(va[3], a0, s1); s1 = fma(va[4], a1, s1); s1 = fma(va[5], a2, s1);
-      s2 = fma(va[6], a0, s2); s2 = fma(va[7], a1, s2); s2 = fma(va[8], a2, s2);
-      if (two) {
-        const double* xb = x + 3 * (int64_t)cb;
-        const double b0 = __ldg(xb), b1 = __ldg(xb + 1), b2 = __ldg(xb + 2);
-        s0 = fma(vb[0], b0, s0); s0 = fma(vb[1], b1, s0); s0 = fma(vb[2], b2, s0);
-        s1 = fma(vb[3], b0, s1); s1 = fma(vb[4], b1, s1); s1 = fma(vb[5], b2, s1);
-        s2 = fma(vb[6], b0, s2); s2 = fma(vb[7], b1, s2); s2 = fma(vb[8], b2, s2);
-      }
+    for (int e = 0; e < 9; ++e) {
+      va[e] = __ldcs(val + e * ns + 32 * t);
+      vb[e] = __ldcs(val + e * ns + 32 * (t + 1));
     }
+    const double* xa = x + 3 * (int64_t)ca;
+    const double* xb = x + 3 * (int64_t)cb;
+    const double a0 = __ldg(xa), a1 = __ldg(xa + 1), a2 = __ldg(xa + 2);
+    const double b0 = __ldg(xb), b1 = __ldg(xb + 1), b2 = __ldg(xb + 2);
+    s0 = fma(va[0], a0, s0); s0 = fma(va[1], a1, s0); s0 = fma(va[2], a2, s0);
+    s1 = fma(va[3], a0, s1); s1 = fma(va[4], a1, s1); s1 = fma(va[5], a2, s1);
+    s2 = fma(va[6], a0, s2); s2 = fma(va[7], a1, s2); s2 = fma(va[8], a2, s2);
+    s0 = fma(vb[0], b0, s0); s0 = fma(vb[1], b1, s0); s0 = fma(vb[2], b2, s0);
+    s1 = fma(vb[3], b0, s1); s1 = fma(vb[4], b1, s1); s1 = fma(vb[5], b2, s1);
+    s2 = fma(vb[6], b0, s2); s2 = fma(vb[7], b1, s2); s2 = fma(vb[8], b2, s2);
   }
+  if (t < width) {
+    const int32_t ca = __ldcs(col + 32 * t);
+    double va[9];
 #pragma unroll
-  for (int o = kBsrLanes / 2; o > 0; o >>= 1) {
-    s0 += __shfl_xor_sync(kFull, s0, o);
-    s1 += __shfl_xor_sync(kFull, s1, o);
-    s2 += __shfl_xor_sync(kFull, s2, o);
+    for (int e = 0; e < 9; ++e) va[e] = __ldcs(val + e * ns + 32 * t);
+    const double* xa = x + 3 * (int64_t)ca;
+    const double a0 = __ldg(xa), a1 = __ldg(xa + 1), a2 = __ldg(xa + 2);
+    s0 = fma(va[0], a0, s0); s0 = fma(va[1], a1, s0); s0 = fma(va[2], a2, s0);
+    s1 = fma(va[3], a0, s1); s1 = fma(va[4], a1, s1); s1 = fma(va[5], a2, s1);
+    s2 = fma(va[6], a0, s2); s2 = fma(va[7], a1, s2); s2 = fma(va[8], a2, s2);
   }
 }
 
 __global__ void __launch_bounds__(kSpmvThreads) k_bsr3_spmv(const rk_csr A, const double* __restrict__ x,
                                                             double* __restrict__ y) {
-  constexpr int RPB = kSpmvThreads / kBsrLanes;  // block rows per thread block pass
-  const int sub = threadIdx.x % kBsrLanes;
+  const int lane = threadIdx.x & 31;
   const int64_t nbr = A.n / 3;
-  for (int64_t base = (int64_t)blockIdx.x * RPB; base < nbr; base += (int64_t)gridDim.x * RPB) {
-    const int64_t br = base + threadIdx.x / kBsrLanes;
+  const int64_t nsl = (nbr + 31) / 32;
+  const int64_t wpb = kSpmvThreads / 32;
+  for (int64_t sl = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); sl < nsl; sl += (int64_t)gridDim.x * wpb) {
     double s0, s1, s2;
-    bsr3_row(A, x, br, br < nbr, sub, s0, s1, s2);
-    if (br < nbr && sub < 3) y[3 * br + sub] = sub == 0 ? s0 : (sub == 1 ? s1 : s2);
+    sell3_row(A, x, sl, lane, s0, s1, s2);
+    const int64_t br = sl * 32 + lane;
+    if (br < nbr) {
+      y[3 * br] = s0;
+      y[3 * br + 1] = s1;
+      y[3 * br + 2] = s2;
+    }
   }
 }
 
@@ -341,21 +343,27 @@ __global__ void __launch_bounds__(kSpmvThreads) k_bsr3_spmv_pcg(const rk_pcg_pla
   const int64_t k = P.st->k;
   const double* __restrict__ p = P.V + k * P.ldv;
   double* __restrict__ Ap = P.AV + (P.ldav ? k * P.ldav : 0);
-  constexpr int RPB = kSpmvThreads / kBsrLanes;
-  const int sub = threadIdx.x % kBsrLanes;
+  const int lane = threadIdx.x & 31;
   const int64_t nbr = P.n / 3;
+  const int64_t nsl = (nbr + 31) / 32;
+  const int64_t wpb = kSpmvThreads / 32;
   double acc[2] = {0.0, 0.0};
-  for (int64_t base = (int64_t)blockIdx.x * RPB; base < nbr; base += (int64_t)gridDim.x * RPB) {
-    const int64_t br = base + threadIdx.x / kBsrLanes;
+  for (int64_t sl = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); sl < nsl; sl += (int64_t)gridDim.x * wpb) {
     double s0, s1, s2;
-    bsr3_row(P.A, p, br, br < nbr, sub, s0, s1, s2);
-    if (br < nbr && sub < 3) {
-      const double s = sub == 0 ? s0 : (sub == 1 ? s1 : s2);
-      const int64_t row = 3 * br + sub;
-      Ap[row] = s;
-      const double pr = p[row];
-      acc[0] = fma(pr, s, acc[0]);
-      acc[1] = fma(pr, pr, acc[1]);
+    sell3_row(P.A, p, sl, lane, s0, s1, s2);
+    const int64_t br = sl * 32 + lane;
+    if (br < nbr) {
+      const int64_t row = 3 * br;
+      Ap[row] = s0;
+      Ap[row + 1] = s1;
+      Ap[row + 2] = s2;
+      const double p0 = p[row], p1 = p[row + 1], p2 = p[row + 2];
+      acc[0] = fma(p0, s0, acc[0]);
+      acc[0] = fma(p1, s1, acc[0]);
+      acc[0] = fma(p2, s2, acc[0]);
+      acc[1] = fma(p0, p0, acc[1]);
+      acc[1] = fma(p1, p1, acc[1]);
+      acc[1] = fma(p2, p2, acc[1]);
     }
   }
   block_sum<2>(acc, scratch);
@@ -366,10 +374,13 @@ __global__ void __launch_bounds__(kSpmvThreads) k_bsr3_spmv_pcg(const rk_pcg_pla
   }
 }
 
+// Slot values from CSR values; perm < 0 marks padding (value 0).
 __global__ void k_bsr3_gather(int64_t total, const int32_t* __restrict__ perm, const double* __restrict__ val,
                               double* __restrict__ bval) {
-  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < total; s += (int64_t)gridDim.x * blockDim.x)
-    bval[s] = __ldg(val + __ldg(perm + s));
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < total; s += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t q = __ldg(perm + s);
+    bval[s] = q >= 0 ? __ldg(val + q) : 0.0;
+  }
 }
 
 }  // namespace rk
@@ -387,8 +398,7 @@ static int resident_blocks(const void* kern, int threads) {
 
 static int launch_bsr3_spmv(const rk_csr& A, const double* x, double* y, cudaStream_t s) {
   static const int cap = resident_blocks((const void*)rk::k_bsr3_spmv, rk::kSpmvThreads);
-  const int64_t rpb = rk::kSpmvThreads / rk::kBsrLanes;
-  const int64_t need = (A.n / 3 + rpb - 1) / rpb;
+  const int64_t need = ((A.n / 3 + 31) / 32 + rk::kSpmvThreads / 32 - 1) / (rk::kSpmvThreads / 32);
   rk::k_bsr3_spmv<<<(int)std::max<int64_t>(1, std::min<int64_t>(cap, need)), rk::kSpmvThreads, 0, s>>>(A, x, y);
   rkh::note_launch();
   return cuda_check("rk_spmv (bsr3)");
@@ -396,8 +406,7 @@ static int launch_bsr3_spmv(const rk_csr& A, const double* x, double* y, cudaStr
 
 static void launch_bsr3_spmv_pcg(const rk_pcg_plan& P, cudaStream_t s) {
   static const int cap = std::min(resident_blocks((const void*)rk::k_bsr3_spmv_pcg, rk::kSpmvThreads), sm_count() * 8);
-  const int64_t rpb = rk::kSpmvThreads / rk::kBsrLanes;
-  const int64_t need = (P.n / 3 + rpb - 1) / rpb;
+  const int64_t need = ((P.n / 3 + 31) / 32 + rk::kSpmvThreads / 32 - 1) / (rk::kSpmvThreads / 32);
   rk::k_bsr3_spmv_pcg<<<(int)std::max<int64_t>(1, std::min<int64_t>(cap, need)), rk::kSpmvThreads, 0, s>>>(P);
   rkh::note_launch();
 }

@@ -191,12 +191,18 @@ _pattern_cache: list = []  # [(host rowptr, host col, _Pattern)]
 USE_BSR3 = os.environ.get("RK_BSR", "1") != "0"
 
 
-class _Bsr3:
-    """3x3 block view of a CSR pattern: block row pointers, block columns and
-    the permutation that gathers CSR values into structure-of-arrays blocks."""
+SELL_SLICE = 32  # block rows per slice (one warp, one block row per lane)
 
-    def __init__(self, browptr, bcol, perm, nblk):
+
+class _Bsr3:
+    """Sliced-ELL view of a 3x3-block pattern (SELL-32 of 3x3 blocks): slice
+    offsets (in slots), the block column of every slot and the permutation that
+    gathers CSR values into structure-of-arrays slot values (-1 = padding).
+    ``nblk`` is the number of slots (real blocks + padding)."""
+
+    def __init__(self, browptr, bcol, perm, nblk, nreal):
         self.browptr, self.bcol, self.perm, self.nblk = browptr, bcol, perm, int(nblk)
+        self.nreal = int(nreal)
 
 
 class _Pattern:
@@ -231,12 +237,27 @@ def _bsr3_from_host(rp: np.ndarray, ci: np.ndarray, n: int, device) -> _Bsr3 | N
     for a in (1, 2):
         if not np.array_equal(t[first[a] // 3 + t_loc, 0] // 3, bcol):
             return None
-    perm = np.empty(9 * nblk, dtype=np.int64)
+    # slices of 32 block rows, each padded to its widest row; slot (s, t, lane)
+    nsl = (nbr + SELL_SLICE - 1) // SELL_SLICE
+    nb_pad = np.zeros(nsl * SELL_SLICE, dtype=np.int64)
+    nb_pad[:nbr] = nb_per
+    width = nb_pad.reshape(nsl, SELL_SLICE).max(axis=1)
+    sptr = np.zeros(nsl + 1, dtype=np.int64)
+    np.cumsum(width * SELL_SLICE, out=sptr[1:])
+    nslot = int(sptr[-1])
+    slot = sptr[b_row // SELL_SLICE] + t_loc * SELL_SLICE + (b_row % SELL_SLICE)
+    scol = np.empty(nslot, dtype=np.int64)
+    # padding slots point at a valid block column (the lane's own row, clamped)
+    sl_of = np.repeat(np.arange(nsl, dtype=np.int64), width * SELL_SLICE)
+    pos = np.arange(nslot, dtype=np.int64) - sptr[sl_of]
+    scol[:] = np.minimum(sl_of * SELL_SLICE + pos % SELL_SLICE, nbr - 1)
+    scol[slot] = bcol
+    perm = np.full(9 * nslot, -1, dtype=np.int64)
     for a in range(3):
         for c in range(3):
-            perm[(3 * a + c) * nblk : (3 * a + c + 1) * nblk] = first[a] + 3 * t_loc + c
+            perm[(3 * a + c) * nslot + slot] = first[a] + 3 * t_loc + c
     to = lambda arr: torch.from_numpy(np.ascontiguousarray(arr, dtype=np.int32)).to(device)  # noqa: E731
-    return _Bsr3(to(browptr), to(bcol), to(perm), nblk)
+    return _Bsr3(to(sptr), to(scol), to(perm), nslot, nblk)
 
 
 def _pattern_known(rowptr: np.ndarray, col: np.ndarray, device) -> bool:
@@ -317,7 +338,7 @@ class SparseSpdMatrix:
         self._csr = nat.RkCsr(self.n, self.nnz, rp.data_ptr(), ci.data_ptr(), vals.data_ptr(), self.lanes, 0)
         self.bval = None
         bsr = pattern.bsr
-        if bsr is not None and bsr.nblk * 9 == self.nnz:
+        if bsr is not None and bsr.nreal * 9 == self.nnz:
             # 3x3 block values for the SpMV kernels (one gather per matrix)
             self.bval = torch.empty(9 * bsr.nblk, dtype=F64, device=self.device)
             nat.check(nat.lib().rk_bsr3_gather(bsr.nblk, bsr.perm.data_ptr(), vals.data_ptr(), self.bval.data_ptr(),
