@@ -26,6 +26,8 @@ __global__ void __launch_bounds__(kGemvThreads) k_gemv_t_partial(
     int64_t n, int64_t m_host, const int64_t* m_dev, const int64_t* done, const double* __restrict__ B,
     int64_t ldb, const double* __restrict__ x, int64_t x_col_from_m, int64_t ldx, double* __restrict__ partials,
     int64_t nchunks) {
+  pdl_wait();
+  pdl_trigger();
   if (done && *done) return;
   const int64_t m = m_dev ? *m_dev : m_host;
   const int64_t c0 = (int64_t)blockIdx.y * kGemvCols;
@@ -56,6 +58,8 @@ __global__ void __launch_bounds__(256) k_gemv_t_reduce(int64_t m_host, const int
                                                        const double* __restrict__ partials,
                                                        int64_t nchunks, const double* __restrict__ div,
                                                        double* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   if (done && *done) return;
   const int64_t m = m_dev ? *m_dev : m_host;
   const int lane = threadIdx.x & 31;
@@ -76,6 +80,8 @@ __global__ void __launch_bounds__(256) k_gemv_n(int64_t n, int64_t m_host, const
                                                 int64_t ldb, const double* __restrict__ c,
                                                 const double* y0, double* y, int64_t y_col_from_m,
                                                 int64_t ldy) {
+  pdl_wait();
+  pdl_trigger();
   if (done && *done) return;
   const int64_t m = m_dev ? *m_dev : m_host;
   extern __shared__ double cs[];
@@ -157,10 +163,10 @@ void launch_gemv_t(int64_t n, int64_t m_max, const int64_t* m_dev, const int64_t
   if (m_max <= 0 || n <= 0) return;
   const int64_t nch = gemv_nchunks(n);
   dim3 g1((unsigned)nch, (unsigned)((m_max + rk::kGemvCols - 1) / rk::kGemvCols));
-  rk::k_gemv_t_partial<<<g1, rk::kGemvThreads, 0, s>>>(n, m_max, m_dev, done, B, ldb, x, x_col_from_m,
-                                                       ldx, partials, nch); rkh::note_launch();
+  launch_pdl(rk::k_gemv_t_partial, g1, dim3(rk::kGemvThreads), 0, s, n, m_max, m_dev, done, B, ldb, x,
+             x_col_from_m, ldx, partials, nch);
   const int64_t g2 = (m_max + 7) / 8;
-  rk::k_gemv_t_reduce<<<(unsigned)g2, 256, 0, s>>>(m_max, m_dev, done, partials, nch, div, out); rkh::note_launch();
+  launch_pdl(rk::k_gemv_t_reduce, dim3((unsigned)g2), dim3(256), 0, s, m_max, m_dev, done, partials, nch, div, out);
 }
 
 void launch_gemv_n(int64_t n, int64_t m_max, const int64_t* m_dev, const int64_t* done, const double* B,
@@ -170,11 +176,14 @@ void launch_gemv_n(int64_t n, int64_t m_max, const int64_t* m_dev, const int64_t
   const size_t smem = (size_t)std::max<int64_t>(m_max, 1) * sizeof(double);
   const int grid = elementwise_grid(n);
   if (op == 0) {
-    rk::k_gemv_n<0><<<grid, 256, smem, s>>>(n, m_max, m_dev, done, B, ldb, c, y0, y, y_col_from_m, ldy); rkh::note_launch();
+    launch_pdl(rk::k_gemv_n<0>, dim3(grid), dim3(256), smem, s, n, m_max, m_dev, done, B, ldb, c, y0, y,
+               y_col_from_m, ldy);
   } else if (op == 1) {
-    rk::k_gemv_n<1><<<grid, 256, smem, s>>>(n, m_max, m_dev, done, B, ldb, c, y0, y, y_col_from_m, ldy); rkh::note_launch();
+    launch_pdl(rk::k_gemv_n<1>, dim3(grid), dim3(256), smem, s, n, m_max, m_dev, done, B, ldb, c, y0, y,
+               y_col_from_m, ldy);
   } else {
-    rk::k_gemv_n<2><<<grid, 256, smem, s>>>(n, m_max, m_dev, done, B, ldb, c, y0, y, y_col_from_m, ldy); rkh::note_launch();
+    launch_pdl(rk::k_gemv_n<2>, dim3(grid), dim3(256), smem, s, n, m_max, m_dev, done, B, ldb, c, y0, y,
+               y_col_from_m, ldy);
   }
 }
 

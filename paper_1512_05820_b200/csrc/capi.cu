@@ -60,6 +60,14 @@ static ProfState g_prof;
 static std::atomic<int64_t> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("RK_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool prof_sample() {
   static uint64_t counter = 0;
   return g_prof.on && ((counter++ & 7u) == 0);

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/podcg.h"
 
 namespace rk {
@@ -72,6 +74,13 @@ __device__ __forceinline__ void combine_partials(const double* partials, int nb,
   __syncthreads();
 }
 
+// Programmatic dependent launch (sm_90+): a kernel launched with programmatic
+// stream serialisation may start while its predecessor drains; it must wait
+// for the predecessor's completion (and memory) before touching its outputs,
+// and lets its own dependents launch early. Both are no-ops without PDL.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" :::); }
+
 // Marks a ticket-synchronised completion without data (used to advance state).
 __device__ __forceinline__ bool ticket_last(uint32_t* ticket) {
   __shared__ bool s_last;
@@ -95,6 +104,30 @@ void note_launch();  // process-wide count of kernels launched (rk_launch_count)
 int cuda_check(const char* where);
 int sm_count();
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+bool pdl_enabled();  // RK_PDL=0 disables programmatic dependent launch
+
+// Launch with programmatic stream serialisation (the kernel must call
+// rk::pdl_wait() before reading its predecessor's results).
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  if (pdl_enabled()) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  } else {
+    kern<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+  }
+  note_launch();
+}
 }  // namespace rkh
 
 #define RK_REQUIRE(cond, code, ...)      \

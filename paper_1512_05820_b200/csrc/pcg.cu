@@ -93,6 +93,8 @@ __device__ __forceinline__ double* r_out(const rk_pcg_plan& P, int64_t k) { retu
 // loads, 16 in flight per lane). Partials: part[v * nchunks + chunk].
 __global__ void __launch_bounds__(kUpdThreads) k_pcg_update(const rk_pcg_plan P, int entry) {
   rk_pcg_state* st = P.st;
+  pdl_wait();
+  pdl_trigger();
   if (st->done) return;
   __shared__ __align__(16) double zs[kProjChunk];
   __shared__ double scratch[64];
@@ -185,6 +187,8 @@ __global__ void __launch_bounds__(kUpdThreads) k_pcg_update(const rk_pcg_plan P,
 // last block to finish, record ||r||, test convergence, form beta and solve mu.
 __global__ void __launch_bounds__(256) k_pcg_finish(const rk_pcg_plan P, int entry, int64_t nchunks) {
   rk_pcg_state* st = P.st;
+  pdl_wait();
+  pdl_trigger();
   if (st->done) return;
   extern __shared__ double dyn[];      // red[2 + m] | ysm[2 w] | Ls[w*w]
   const int64_t m = P.m;
@@ -249,6 +253,8 @@ __global__ void __launch_bounds__(256) k_pcg_finish(const rk_pcg_plan P, int ent
 // K5: new direction into V[:, k+1] (entry: V[:, 0]).
 __global__ void __launch_bounds__(256) k_pcg_direction(const rk_pcg_plan P, int entry) {
   rk_pcg_state* st = P.st;
+  pdl_wait();
+  pdl_trigger();
   if (st->done) return;
   extern __shared__ double sm[];
   const int64_t k = st->k;
@@ -355,15 +361,15 @@ static void launch_update(const rk_pcg_plan& P, int entry, cudaStream_t s) {
   const int64_t nch = update_chunks(P.n);
   const int64_t groups = std::max<int64_t>(1, (P.m + rk::kProjCols - 1) / rk::kProjCols);
   dim3 grid((unsigned)nch, (unsigned)groups);
-  rk::k_pcg_update<<<grid, rk::kUpdThreads, 0, s>>>(P, entry); rkh::note_launch();
+  launch_pdl(rk::k_pcg_update, grid, dim3(rk::kUpdThreads), 0, s, P, entry);
   const int64_t nv = 2 + P.m;
   const unsigned fgrid = (unsigned)((nv + 7) / 8);
-  rk::k_pcg_finish<<<fgrid, 256, finish_smem(P.m, P.wchol), s>>>(P, entry, nch); rkh::note_launch();
+  launch_pdl(rk::k_pcg_finish, dim3(fgrid), dim3(256), finish_smem(P.m, P.wchol), s, P, entry, nch);
 }
 
 static void launch_direction(const rk_pcg_plan& P, int entry, int64_t kmax, cudaStream_t s) {
   const size_t smem = (size_t)(P.m + (P.mode == 2 ? kmax + 1 : 0) + 1) * sizeof(double);
-  rk::k_pcg_direction<<<elementwise_grid(P.n), 256, smem, s>>>(P, entry); rkh::note_launch();
+  launch_pdl(rk::k_pcg_direction, dim3(elementwise_grid(P.n)), dim3(256), smem, s, P, entry);
   if (P.mode == 1 && !entry) {
     // two classical Gram-Schmidt sweeps against every previous direction
     // (krylov.py:333-337, block form): coef_i = (A p_i)'p / gamma_i ; p -= V coef

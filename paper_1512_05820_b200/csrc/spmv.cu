@@ -102,6 +102,8 @@ __device__ __forceinline__ void curvature_epilogue(const rk_pcg_plan& P, double 
 // K1 fused: Ap_k = A p_k with gamma = p'Ap and p'p reduced in the same pass.
 template <int LANES>
 __global__ void __launch_bounds__(kSpmvThreads) k_spmv_pcg(const rk_pcg_plan P) {
+  pdl_wait();
+  pdl_trigger();
   if (P.st->done) return;
   constexpr int RPB = kSpmvThreads / LANES;
   __shared__ double scratch[64];
@@ -135,6 +137,8 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv_pcg(const rk_pcg_plan P) 
 
 // Generic-operator variant: the caller already wrote A p_k; reduce gamma, p'p.
 __global__ void __launch_bounds__(kSpmvThreads) k_curvature(const rk_pcg_plan P) {
+  pdl_wait();
+  pdl_trigger();
   if (P.st->done) return;
   __shared__ double scratch[64];
   const int64_t k = P.st->k;
@@ -338,6 +342,8 @@ __global__ void __launch_bounds__(kSpmvThreads) k_bsr3_spmv(const rk_csr A, cons
 }
 
 __global__ void __launch_bounds__(kSpmvThreads) k_bsr3_spmv_pcg(const rk_pcg_plan P) {
+  pdl_wait();
+  pdl_trigger();
   if (P.st->done) return;
   __shared__ double scratch[64];
   const int64_t k = P.st->k;
@@ -407,8 +413,8 @@ static int launch_bsr3_spmv(const rk_csr& A, const double* x, double* y, cudaStr
 static void launch_bsr3_spmv_pcg(const rk_pcg_plan& P, cudaStream_t s) {
   static const int cap = std::min(resident_blocks((const void*)rk::k_bsr3_spmv_pcg, rk::kSpmvThreads), sm_count() * 8);
   const int64_t need = ((P.n / 3 + 31) / 32 + rk::kSpmvThreads / 32 - 1) / (rk::kSpmvThreads / 32);
-  rk::k_bsr3_spmv_pcg<<<(int)std::max<int64_t>(1, std::min<int64_t>(cap, need)), rk::kSpmvThreads, 0, s>>>(P);
-  rkh::note_launch();
+  launch_pdl(rk::k_bsr3_spmv_pcg, dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(cap, need))),
+             dim3(rk::kSpmvThreads), 0, s, P);
 }
 
 int launch_bsr3_gather(int64_t nblk, const int32_t* perm, const double* val, double* bval, cudaStream_t s) {
@@ -471,7 +477,7 @@ template <int L>
 static void launch_spmv_pcg_l(const rk_pcg_plan& P, cudaStream_t s) {
   static const int cap = std::min(resident_grid(rk::k_spmv_pcg<L>, rk::kSpmvThreads, INT64_MAX), sm_count() * 8);
   const int grid = (int)std::min<int64_t>(cap, (P.n + rk::kSpmvThreads / L - 1) / (rk::kSpmvThreads / L));
-  rk::k_spmv_pcg<L><<<std::max(grid, 1), rk::kSpmvThreads, 0, s>>>(P); rkh::note_launch();
+  launch_pdl(rk::k_spmv_pcg<L>, dim3(std::max(grid, 1)), dim3(rk::kSpmvThreads), 0, s, P);
 }
 
 void launch_spmv_pcg(const rk_pcg_plan& P, cudaStream_t s) {
@@ -495,7 +501,7 @@ int curvature_grid(int64_t n) {
 }
 
 void launch_curvature(const rk_pcg_plan& P, cudaStream_t s) {
-  rk::k_curvature<<<curvature_grid(P.n), 256, 0, s>>>(P); rkh::note_launch();
+  launch_pdl(rk::k_curvature, dim3(curvature_grid(P.n)), dim3(256), 0, s, P);
 }
 
 template <int L>
