@@ -136,6 +136,8 @@ int64_t rk_pcg_workspace_doubles(int64_t n, int64_t m, int64_t vcap);
 int64_t rk_reduce_workspace_doubles(int64_t n, int64_t m);
 /* Doubles of split-K workspace rk_gram needs. */
 int64_t rk_gram_workspace_doubles(int64_t n, int64_t m1, int64_t m2);
+/* Doubles of split-K workspace rk_gram_upper needs for the same col_off. */
+int64_t rk_gram_upper_workspace_doubles(int64_t n, int64_t m1, int64_t m2, int64_t col_off);
 
 /* ---- augmented PCG (krylov.py:181-345) ------------------------------------ */
 /* Entry: z = M^{-1} r0, rz, ||r0|| into res_h[0], mu = F^{-1} cross'z, p_0 = z - B mu
@@ -200,7 +202,7 @@ int rk_gram(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m2,
  * is global column b + col_off (row a is global row a): 64x64 tiles strictly below
  * the diagonal are skipped and left undefined; the caller mirrors the upper part.
  * Halves the flops of the POD snapshot Gram S'(AS) (pod.py:119, symmetrised by
- * the reference at pod.py:129 anyway). */
+ * the reference at pod.py:129 anyway). ws: rk_gram_upper_workspace_doubles(n, m1, m2, col_off). */
 int rk_gram_upper(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m2,
                   const double* Y, int64_t ldy, int64_t col_off, double* G, int64_t ldg,
                   double* ws, int64_t ws_len, void* stream);

@@ -106,6 +106,7 @@ _SIGNATURES = {
     "rk_pcg_workspace_doubles": (c_i64, [c_i64, c_i64, c_i64]),
     "rk_reduce_workspace_doubles": (c_i64, [c_i64, c_i64]),
     "rk_gram_workspace_doubles": (c_i64, [c_i64, c_i64, c_i64]),
+    "rk_gram_upper_workspace_doubles": (c_i64, [c_i64, c_i64, c_i64, c_i64]),
     "rk_pcg_entry": (c_i32, [ctypes.POINTER(RkPcgPlan), c_vp]),
     "rk_pcg_steps": (c_i32, [ctypes.POINTER(RkPcgPlan), c_i32, c_i64, c_vp]),
     "rk_pcg_curvature": (c_i32, [ctypes.POINTER(RkPcgPlan), c_vp]),

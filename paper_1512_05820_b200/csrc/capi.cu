@@ -113,7 +113,7 @@ void launch_axpby(int64_t n, double a, const double* x, double b, double* y, cud
 void launch_sub_from(int64_t n, const double* x0, double* y, cudaStream_t s);
 int launch_gram(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m2, const double* Y, int64_t ldy,
                 double* G, int64_t ldg, double* ws, int64_t ws_len, int64_t upper_off, cudaStream_t s);
-int64_t gram_workspace_doubles(int64_t n, int64_t m1, int64_t m2);
+int64_t gram_workspace_doubles(int64_t n, int64_t m1, int64_t m2, int64_t upper_off);
 int launch_gemm_nn(int64_t n, int64_t sdim, int64_t y, const double* S, int64_t lds, const double* C, int64_t ldc,
                    double* Out, int64_t ldo, cudaStream_t s);
 
@@ -152,7 +152,12 @@ int64_t rk_reduce_workspace_doubles(int64_t n, int64_t m) {
 }
 
 int64_t rk_gram_workspace_doubles(int64_t n, int64_t m1, int64_t m2) {
-  return rkh::gram_workspace_doubles(n, m1, m2);
+  return rkh::gram_workspace_doubles(n, m1, m2, -1);
+}
+
+int64_t rk_gram_upper_workspace_doubles(int64_t n, int64_t m1, int64_t m2, int64_t col_off) {
+  if (n <= 0 || m1 <= 0 || m2 <= 0 || col_off < 0) return 0;
+  return rkh::gram_workspace_doubles(n, m1, m2, col_off);
 }
 
 int rk_pcg_entry(const rk_pcg_plan* plan, void* stream) {

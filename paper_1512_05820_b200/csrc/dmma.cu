@@ -240,15 +240,44 @@ struct GramGeom {
   int64_t ta, tb, splits, rows_per_split;
 };
 
-static GramGeom gram_geometry(int64_t n, int64_t m1, int64_t m2) {
+// Tiles the kernel computes: all of them, or (upper_off >= 0) those not strictly
+// below the diagonal of the enclosing symmetric matrix.
+static int64_t active_tiles(int64_t ta, int64_t tb, int64_t upper_off) {
+  if (upper_off < 0) return ta * tb;
+  int64_t count = 0;
+  for (int64_t b = 0; b < tb; ++b) {
+    const int64_t last_a = (b * rk::kTile + upper_off + rk::kTile - 1) / rk::kTile;  // a0 <= b0 + off + 63
+    count += std::min(ta, last_a + 1);
+  }
+  return count;
+}
+
+// Split N so the (tile, split) units fill whole waves of the resident CTA slots
+// (2 per SM): each unit is the same amount of work, so the tail of a partial
+// wave is the loss. Picks the fewest waves (<= 8) within 3% of the best fill.
+static GramGeom gram_geometry(int64_t n, int64_t m1, int64_t m2, int64_t upper_off) {
   GramGeom g;
   g.ta = (m1 + rk::kTile - 1) / rk::kTile;
   g.tb = (m2 + rk::kTile - 1) / rk::kTile;
-  const int64_t tiles = std::max<int64_t>(1, g.ta * g.tb);
-  const int64_t target = (int64_t)sm_count() * 2;
-  int64_t splits = (target + tiles - 1) / tiles;
+  const int64_t tiles = std::max<int64_t>(1, active_tiles(g.ta, g.tb, upper_off));
+  const int64_t slots = (int64_t)sm_count() * 2;
   const int64_t max_splits = std::max<int64_t>(1, n / 512);
-  splits = std::max<int64_t>(1, std::min(splits, max_splits));
+  double fill[9] = {0};
+  int64_t pick[9] = {0};
+  double best = 0.0;
+  for (int w = 1; w <= 8; ++w) {
+    const int64_t sp = std::max<int64_t>(1, std::min(max_splits, slots * w / tiles));
+    const int64_t units = sp * tiles;
+    fill[w] = (double)units / (double)(slots * ((units + slots - 1) / slots));
+    pick[w] = sp;
+    best = std::max(best, fill[w]);
+  }
+  int64_t splits = pick[8];
+  for (int w = 1; w <= 8; ++w)
+    if (fill[w] >= best - 0.03) {
+      splits = pick[w];
+      break;
+    }
   int64_t rps = (n + splits - 1) / splits;
   rps = (rps + rk::kStep - 1) / rk::kStep * rk::kStep;
   splits = std::max<int64_t>(1, (n + rps - 1) / rps);
@@ -257,8 +286,8 @@ static GramGeom gram_geometry(int64_t n, int64_t m1, int64_t m2) {
   return g;
 }
 
-int64_t gram_workspace_doubles(int64_t n, int64_t m1, int64_t m2) {
-  const GramGeom g = gram_geometry(n, m1, m2);
+int64_t gram_workspace_doubles(int64_t n, int64_t m1, int64_t m2, int64_t upper_off) {
+  const GramGeom g = gram_geometry(std::max<int64_t>(n, 1), m1, m2, upper_off);
   return g.splits > 1 ? g.splits * m1 * m2 : 0;
 }
 
@@ -275,7 +304,7 @@ int launch_gram(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m2,
     cudaFuncSetAttribute(rk::k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem());
     configured = true;
   }
-  const GramGeom g = gram_geometry(std::max<int64_t>(n, 1), m1, m2);
+  const GramGeom g = gram_geometry(std::max<int64_t>(n, 1), m1, m2, upper_off);
   dim3 grid((unsigned)g.ta, (unsigned)g.tb, (unsigned)g.splits);
   if (g.splits == 1) {
     rk::k_gram<<<grid, rk::kDmmaThreads, gram_smem(), s>>>(n, m1, X, ldx, m2, Y, ldy, G, ldg, 0, g.rows_per_split,

@@ -560,7 +560,7 @@ def symmetric_gram_from_products(Z: torch.Tensor, products, col_scale=None) -> U
         w = int(AB.shape[1])
         if w == 0:
             continue
-        ws = s.workspace(max(nat.lib().rk_gram_workspace_doubles(n, m, w), 1))
+        ws = s.workspace(max(nat.lib().rk_gram_upper_workspace_doubles(n, m, w, off), 1))
         Gblk = store[off : off + w]  # rows of the row-major store = columns of G
         nat.check(nat.lib().rk_gram_upper(n, m, Z.data_ptr(), block_ld(Z), w, AB.data_ptr(), block_ld(AB), off,
                                           Gblk.data_ptr(), m, ws.data_ptr(), ws.numel(), nat.stream_ptr(dev)),
