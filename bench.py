@@ -230,8 +230,8 @@ def run_b200(args, rank, world, dist):
             e1.record(stream)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
-    ms = (ctypes.c_double * 3)()
-    cnt = (ctypes.c_int64 * 3)()
+    ms = (ctypes.c_double * 4)()
+    cnt = (ctypes.c_int64 * 4)()
     lib.rk_profile_end(ms, cnt)
     launches = (lib.rk_launch_count() - launches0) / max(args.steps, 1)
     t_step = max_over_ranks(float(np.mean(times)), dist)
@@ -258,7 +258,7 @@ def run_b200(args, rank, world, dist):
                "path": "run_sequence over host CSR (reference-style SparseSpdMatrix fields), solutions copied back"}
         del xh
 
-    avg = [ms[i] / max(cnt[i], 1) for i in range(3)]
+    avg = [ms[i] / max(cnt[i], 1) for i in range(4)]
     peaks = _peaks()
     A0 = dev_specs[0].A
     if A0.bval is not None:
@@ -308,7 +308,8 @@ def run_b200(args, rank, world, dist):
             "peak_source": peaks["source"],
         },
         "kernels_ms_avg": {"spmv_pcg": round(avg[0], 4), "pcg_update": round(avg[1], 4),
-                           "pcg_direction": round(avg[2], 4), "launches": list(cnt)},
+                           "pcg_finish": round(avg[2], 4), "pcg_direction": round(avg[3], 4),
+                           "launches": list(cnt)},
         "sequence": {"stage3_iters_total": int(sum(iters)), "cg_iters_per_s": round(sum(iters) / t_step, 1),
                      "per_system_iters": iters, "q_last": q_last,
                      "all_converged": bool(all(r.converged for r in reports))},

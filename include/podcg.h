@@ -56,10 +56,10 @@ typedef struct rk_csr {
    * slice, padded to the slice's widest row). When bval != NULL the SpMV
    * kernels stream 9 values + 1 block index per stored block instead of
    * 9 x (value + index), i.e. 76 instead of 108 bytes per 9 nonzeros.
-   * Slot (slice s, position t, lane l) = browptr[s] + 32 t + l. Values are
-   * structure-of-arrays: bval[e * nblk + slot] is entry e = 3*a + c (row a,
-   * column c) of the block in that slot (0 for padding); rk_bsr3_gather fills
-   * them from val. */
+   * Slot (slice s, position t, lane l) = browptr[s] + 32 t + l. Values come
+   * in one contiguous 9 x 32 tile per slot row: entry e = 3*a + c (row a,
+   * column c) of the block in slot q is bval[9 * (q - q % 32) + 32 e + q % 32]
+   * (0 for padding); rk_bsr3_gather fills them from val. */
   int64_t nblk;           /* number of slots (stored blocks + padding) */
   const int32_t* browptr; /* ceil(n/96) + 1 slice offsets, in slots */
   const int32_t* bcol;    /* nblk block columns (padding: a valid column) */
@@ -90,6 +90,9 @@ typedef struct rk_pcg_state {
  *   K5  p_{k+1} = z + beta p_k - B mu  (cg)                     (krylov.py:323-326)
  *       p_{k+1} = z - B mu, then 2 block-CGS sweeps (fom)       (krylov.py:327-337)
  *       p_{k+1} = z - B mu + sum_i rz'/rz_i p_i  (fom, paper beta) (krylov.py:329-331) */
+/* Counters a PCG plan's ticket array holds (0-3 kernel tickets, 8.. chunk groups). */
+#define RK_PCG_TICKETS 272
+
 typedef struct rk_pcg_plan {
   int64_t n;
   rk_csr A;                 /* A.rowptr == NULL: generic operator, caller fills AV */
@@ -122,7 +125,7 @@ typedef struct rk_pcg_plan {
   double* res_h;            /* vcap + 1: residual norms, res_h[0] = ||r_0|| */
   double* partials;         /* workspace, rk_pcg_workspace_doubles() */
   int64_t partials_len;
-  uint32_t* tickets;        /* 8 zero-initialised counters */
+  uint32_t* tickets;        /* RK_PCG_TICKETS zero-initialised counters */
   int32_t mode;             /* 0 cg, 1 fom (two CGS sweeps), 2 fom with paper beta */
   int32_t pad_;
 } rk_pcg_plan;
@@ -229,7 +232,10 @@ int rk_pod_coef(int64_t m, int64_t y, const double* V, int64_t ldv, const double
 int rk_profile_begin(void);
 /* Number of kernels this library has launched since it was loaded. */
 int64_t rk_launch_count(void);
-int rk_profile_end(double* ms3, int64_t* count3);
+/* Debug: copies up to n of the 64 x 8 globaltimer stamps of the fused update
+ * tail (iteration k in row k % 64); zeros unless built with -DRK_TAIL_TRACE. */
+int rk_debug_trace(uint64_t* out, int64_t n);
+int rk_profile_end(double* ms4, int64_t* count4);  /* slots: spmv, update, finish, direction */
 
 #ifdef __cplusplus
 }

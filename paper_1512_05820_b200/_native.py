@@ -15,7 +15,7 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libpodcg.so")
+LIB_PATH = os.environ.get("RK_LIB") or os.path.join(_HERE, "_lib", "libpodcg.so")
 
 c_i64 = ctypes.c_int64
 c_i32 = ctypes.c_int32
@@ -99,6 +99,7 @@ class RkPcgPlan(ctypes.Structure):
 
 
 STATE_BYTES = ctypes.sizeof(RkPcgState)
+PCG_TICKETS = 272  # RK_PCG_TICKETS (include/podcg.h)
 
 _SIGNATURES = {
     "rk_last_error": (ctypes.c_char_p, []),
@@ -131,6 +132,7 @@ _SIGNATURES = {
     "rk_pod_coef": (c_i32, [c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "rk_profile_begin": (c_i32, []),
     "rk_launch_count": (c_i64, []),
+    "rk_debug_trace": (c_i32, [ctypes.POINTER(ctypes.c_uint64), c_i64]),
     "rk_profile_end": (c_i32, [ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64)]),
 }
 
@@ -211,7 +213,7 @@ class Scratch:
     def __init__(self, device):
         self.device = device
         self.ws = torch.empty(0, dtype=torch.float64, device=device)
-        self.tickets = torch.zeros(16, dtype=torch.int32, device=device)
+        self.tickets = torch.zeros(PCG_TICKETS, dtype=torch.int32, device=device)
         self.out = torch.zeros(8, dtype=torch.float64, device=device)
 
     def workspace(self, ndoubles: int) -> torch.Tensor:

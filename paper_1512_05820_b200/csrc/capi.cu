@@ -114,6 +114,7 @@ void launch_sub_from(int64_t n, const double* x0, double* y, cudaStream_t s);
 int launch_gram(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m2, const double* Y, int64_t ldy,
                 double* G, int64_t ldg, double* ws, int64_t ws_len, int64_t upper_off, cudaStream_t s);
 int64_t gram_workspace_doubles(int64_t n, int64_t m1, int64_t m2, int64_t upper_off);
+int debug_trace(unsigned long long* out, int64_t n);
 int launch_gemm_nn(int64_t n, int64_t sdim, int64_t y, const double* S, int64_t lds, const double* C, int64_t ldc,
                    double* Out, int64_t ldo, cudaStream_t s);
 
@@ -306,6 +307,11 @@ int rk_gemm_nn(int64_t n, int64_t s, int64_t y, const double* S, int64_t lds, co
 
 extern "C" {
 
+// Debug timeline of the fused update tail (zeros unless built with -DRK_TAIL_TRACE).
+int rk_debug_trace(uint64_t* out, int64_t n) {
+  return rkh::debug_trace(reinterpret_cast<unsigned long long*>(out), n);
+}
+
 // Kernels launched by this library since load (all threads).
 int64_t rk_launch_count(void) { return rkh::g_launches.load(std::memory_order_relaxed); }
 
@@ -318,19 +324,19 @@ int rk_profile_begin(void) {
 }
 
 // Stop; synchronises and writes total milliseconds and launch counts per kernel
-// slot (3 slots: spmv, update, direction).
-int rk_profile_end(double* ms3, int64_t* count3) {
+// slot (4 slots: spmv, update, finish, direction).
+int rk_profile_end(double* ms4, int64_t* count4) {
   rkh::g_prof.on = false;
-  for (int i = 0; i < 3; ++i) { ms3[i] = 0.0; count3[i] = 0; }
+  for (int i = 0; i < 4; ++i) { ms4[i] = 0.0; count4[i] = 0; }
   auto& mk = rkh::g_prof.marks;
   if (!mk.empty() && cudaEventSynchronize(mk.back().second) != cudaSuccess) return rkh::cuda_check("rk_profile_end");
   for (size_t i = 0; i + 1 < mk.size(); ++i) {
     const int a = mk[i].first, b = mk[i + 1].first;
-    if (b == a + 1 && a < 3) {
+    if (b == a + 1 && a < 4) {
       float ms = 0.f;
       if (cudaEventElapsedTime(&ms, mk[i].second, mk[i + 1].second) == cudaSuccess) {
-        ms3[a] += ms;
-        count3[a] += 1;
+        ms4[a] += ms;
+        count4[a] += 1;
       }
     }
   }

@@ -20,6 +20,25 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// N independent butterflies interleaved level by level (ILP across the N
+// values); each result is bitwise what warp_sum gives for that value.
+template <int N>
+__device__ __forceinline__ void warp_sum_n(double (&v)[N]) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double t[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) t[q] = __shfl_xor_sync(kFull, v[q], o);
+#pragma unroll
+    for (int q = 0; q < N; ++q) v[q] += t[q];
+  }
+}
+
+// Release/acquire fence at GPU scope (cheaper than __threadfence's fence.sc):
+// orders this thread's (and, after a barrier, its block's) prior writes before
+// a following ticket atomic, and the ticket before later reads.
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;\n" ::: "memory"); }
+
 // Block-wide sum of NV values; result valid in every thread. scratch >= 32*NV.
 template <int NV>
 __device__ __forceinline__ void block_sum(double (&v)[NV], double* scratch) {

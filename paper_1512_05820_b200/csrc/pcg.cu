@@ -39,10 +39,27 @@ int elementwise_grid(int64_t n);
 
 namespace rk {
 
+// Debug-only timeline of the fused update tail (built with -DRK_TAIL_TRACE):
+// row k % 64 holds globaltimer stamps of iteration k (see rk_debug_trace).
+__device__ unsigned long long g_tail_trace[64 * 8];
+#ifdef RK_TAIL_TRACE
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define RK_STAMP(var) const unsigned long long var = clock64()  // same block: SM cycles
+#else
+#define RK_STAMP(var)
+#endif
+
 constexpr int kUpdThreads = 256;
 constexpr int kProjChunk = 1024;                 // rows per update block
 constexpr int kProjCols = 32;                    // cross columns per update block (4 per warp)
 constexpr int kMaxProj = 2048;                   // projection width of the fused path
+constexpr int kStageFactor = 96;                 // Linv staged in shared memory up to this width
+constexpr int kFuseMax = 64;                     // widths whose finish runs in the update kernel's tail
+constexpr int kMaxGroups = 256;                  // chunk groups of the fused two-level combine
 
 // mu = F^{-1} c with F = blockdiag(L L', diag(sqd)^2) (krylov.py:119-132
 // BlockDiagFactor.solve_spd). P.L holds Linv = L^{-1} (lower triangular, from
@@ -50,13 +67,13 @@ constexpr int kMaxProj = 2048;                   // projection width of the fuse
 // triangular mat-vecs, y = Linv c and mu = Linv' y, one output per thread
 // (instead of a chain of w dependent substitution steps); the diagonal block
 // is a division.
-__device__ void solve_factor(const rk_pcg_plan& P, const double* c, double* ysm, double* Ls, double* mu) {
+__device__ void solve_factor(const rk_pcg_plan& P, const double* c, double* ysm, const double* Ls, double* mu) {
   const int64_t w = P.wchol, m = P.m;
-  // Linv (<= 2048^2 doubles, L2 resident) is read in place: each thread's row
-  // loads are independent, so they are all in flight at once.
-  const double* __restrict__ L = P.L;
-  const int64_t ldl = P.ldl;
-  (void)Ls;
+  // Linv is either staged in shared memory (Ls, ld = w, zero above the
+  // diagonal) or, for wide factors (<= 2048^2 doubles, L2 resident), read in
+  // place: each thread's row loads are independent, so they are all in flight.
+  const double* __restrict__ L = Ls ? Ls : P.L;
+  const int64_t ldl = Ls ? w : P.ldl;
   for (int64_t i = threadIdx.x; i < w; i += blockDim.x) {   // y = Linv c
     double s = 0.0;
     for (int64_t j = 0; j <= i; ++j) s = fma(L[i + j * ldl], c[j], s);
@@ -78,6 +95,140 @@ __device__ void solve_factor(const rk_pcg_plan& P, const double* c, double* ysm,
   }
 }
 
+// mu = F^{-1} c for w <= kFuseMax with one 256-thread block: warp q-rows
+// (rows warp + 8q), lanes over the row's entries, butterfly sums. Each batch of
+// 32 entries issues all its rows' loads before any fma, so a triangular
+// mat-vec costs ceil(w / 32) L2 round trips rather than one per row.
+__device__ void solve_factor_warps(const rk_pcg_plan& P, const double* c, double* y, double* mu) {
+  constexpr int R = kFuseMax / 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int w = (int)P.wchol, m = (int)P.m;
+  const int64_t ldl = P.ldl;
+  const double* __restrict__ L = P.L;
+  double a[R], lv[R];
+#pragma unroll
+  for (int q = 0; q < R; ++q) a[q] = 0.0;
+  for (int t = 0; 32 * t < w; ++t) {  // y_i = sum_{j <= i} Linv[i, j] c_j
+    const int j = lane + 32 * t;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int i = warp + 8 * q;
+      lv[q] = (i < w && j <= i) ? __ldg(L + i + (int64_t)j * ldl) : 0.0;
+    }
+    const double cj = j < w ? c[j] : 0.0;
+#pragma unroll
+    for (int q = 0; q < R; ++q) a[q] = fma(lv[q], cj, a[q]);
+  }
+  warp_sum_n(a);
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const int i = warp + 8 * q;
+    if (lane == 0 && i < w) y[i] = a[q];
+    a[q] = 0.0;
+  }
+  __syncthreads();
+  for (int t = 0; 32 * t < w; ++t) {  // mu_i = sum_{j >= i} Linv[j, i] y_j (column i: coalesced)
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int i = warp + 8 * q;
+      const int j = lane + 32 * t;
+      lv[q] = (i < w && j >= i && j < w) ? __ldg(L + j + (int64_t)i * ldl) : 0.0;
+    }
+    const int j = lane + 32 * t;
+    const double yj = j < w ? y[j] : 0.0;
+#pragma unroll
+    for (int q = 0; q < R; ++q) a[q] = fma(lv[q], yj, a[q]);
+  }
+  warp_sum_n(a);
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const int i = warp + 8 * q;
+    if (lane == 0 && i < w) mu[i] = a[q];
+  }
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    if (i >= w) {
+      const double d = P.sqd[i - w];
+      mu[i] = c[i] / (d * d);
+    }
+  }
+}
+
+// Fixed-order sums out[v] = sum_{c in [c0, c1)} src[v * ld + c] for v < nv
+// (nv <= 2 + kFuseMax) by one 256-thread block: warp-owned values, lanes over
+// c, every value's loads issued together (one L2 round trip per 32 columns).
+__device__ __forceinline__ void block_row_sums(const double* src, int64_t ld, int64_t nv, int64_t c0, int64_t c1,
+                                               double* out, int64_t out_stride) {
+  constexpr int QV = (2 + kFuseMax + 7) / 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double a[QV];
+#pragma unroll
+  for (int q = 0; q < QV; ++q) a[q] = 0.0;
+  for (int64_t c = c0 + lane; c < c1; c += 32) {
+#pragma unroll
+    for (int q = 0; q < QV; ++q) {
+      const int64_t v = warp + 8 * q;
+      if (v < nv) a[q] += __ldcg(src + v * ld + c);
+    }
+  }
+  warp_sum_n(a);
+#pragma unroll
+  for (int q = 0; q < QV; ++q) {
+    const int64_t v = warp + 8 * q;
+    if (lane == 0 && v < nv) out[v * out_stride] = a[q];
+  }
+}
+
+// Scalar bookkeeping of the combined update reductions red = [||r||^2, r'z, c]:
+// history, convergence test, beta (krylov.py:268,292,314-324,340). Returns true
+// when the run stopped (the caller then skips the mu solve). Block-uniform.
+__device__ bool pcg_scalars(const rk_pcg_plan& P, int entry, const double* red) {
+  rk_pcg_state* st = P.st;
+  __shared__ int s_stop;
+  if (threadIdx.x == 0) {
+    const int64_t k = st->k;
+    const double rr = red[0], rz_next = red[1];
+    const double rnorm = sqrt(rr);
+    st->rr = rr;
+    s_stop = 0;
+    if (entry) {
+      // krylov.py:268 history[0] = ||r0|| ; :292 rz = r @ z
+      P.res_h[0] = rnorm;
+      st->rz = rz_next;
+    } else {
+      P.res_h[k + 1] = rnorm;                  // krylov.py:314
+      if (rnorm <= st->threshold) {            // krylov.py:317
+        st->status = 1;
+        st->done = 1;
+        st->k = k + 1;
+        s_stop = 1;
+      } else {
+        st->rz_next = rz_next;                 // krylov.py:321
+        st->beta = rz_next / st->rz;           // krylov.py:324 (rz_next / rz)
+        st->rz = rz_next;                      // krylov.py:340
+      }
+    }
+  }
+  __syncthreads();
+  return s_stop != 0;
+}
+
+// Like ticket_last, for a counter that expects `expected` arrivals.
+__device__ __forceinline__ bool ticket_last_of(uint32_t* ticket, uint32_t expected) {
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    fence_acq_rel_gpu();  // release the block's writes (ordered by the barrier)
+    const uint32_t t = atomicAdd(ticket, 1u);
+    s_last = (t == expected - 1);
+    if (s_last) {
+      *ticket = 0u;
+      fence_acq_rel_gpu();  // acquire: every other block's writes are visible
+    }
+  }
+  __syncthreads();
+  return s_last;
+}
+
 // Residual ping-pong: iteration k reads r_k from buffer k&1 and writes r_{k+1}
 // to the other one, so every block of the 2-D update grid can recompute z for
 // its rows from unmodified inputs (entry reads buffer 0 and writes nothing).
@@ -91,7 +242,7 @@ __device__ __forceinline__ double* r_out(const rk_pcg_plan& P, int64_t k) { retu
 // also writes x, r_{k+1}, z and the ||r||^2, r'z partials. Then each warp
 // reduces 4 columns of cross' z over the chunk (lanes over rows, 16-byte
 // loads, 16 in flight per lane). Partials: part[v * nchunks + chunk].
-__global__ void __launch_bounds__(kUpdThreads) k_pcg_update(const rk_pcg_plan P, int entry) {
+__global__ void __launch_bounds__(kUpdThreads, 4) k_pcg_update(const rk_pcg_plan P, int entry, int fused, int64_t group) {
   rk_pcg_state* st = P.st;
   pdl_wait();
   pdl_trigger();
@@ -99,6 +250,9 @@ __global__ void __launch_bounds__(kUpdThreads) k_pcg_update(const rk_pcg_plan P,
   __shared__ __align__(16) double zs[kProjChunk];
   __shared__ double scratch[64];
   const int64_t k = st->k;
+#ifdef RK_TAIL_TRACE
+  if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) g_tail_trace[(k % 64) * 8 + 0] = gtimer();
+#endif
   const double alpha = entry ? 0.0 : st->alpha;
   const int64_t n = P.n, m = P.m;
   const int64_t nchunks = gridDim.x;
@@ -181,73 +335,81 @@ __global__ void __launch_bounds__(kUpdThreads) k_pcg_update(const rk_pcg_plan P,
     a = warp_sum(a);
     if (lane == 0) part[(2 + j) * nchunks + chunk] = a;
   }
+  if (!fused) return;
+  RK_STAMP(t1);
+  // Fused finish (m <= kFuseMax): the last block of each group of `group`
+  // chunks (over all column groups) sums the group's partials; the last group
+  // sum to land combines the groups, then does the scalars and the mu solve.
+  // Fixed orders throughout (lanes over chunks, butterfly), so deterministic.
+  __shared__ double red[2 + kFuseMax];
+  __shared__ double ysm[kFuseMax];
+  const int64_t nv = 2 + m;
+  const int64_t ngroups = (nchunks + group - 1) / group;
+  const int64_t g = chunk / group;
+  const int64_t c0 = g * group, c1 = min(nchunks, c0 + group);
+  if (!ticket_last_of(P.tickets + 8 + g, (uint32_t)((c1 - c0) * gridDim.y))) return;
+  RK_STAMP(t2);
+  double* gsum = part + nv * nchunks;  // [nv][ngroups]
+  block_row_sums(part, nchunks, nv, c0, c1, gsum + g, ngroups);
+  RK_STAMP(t3);
+  if (!ticket_last_of(P.tickets + 3, (uint32_t)ngroups)) return;
+  RK_STAMP(t4);
+  block_row_sums(gsum, ngroups, nv, 0, ngroups, red, 1);
+  __syncthreads();
+  RK_STAMP(t5);
+  const bool stop = pcg_scalars(P, entry, red);
+  RK_STAMP(t6);
+  if (!stop && m > 0) solve_factor_warps(P, red + 2, ysm, P.mu);
+#ifdef RK_TAIL_TRACE
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long* row = g_tail_trace + (k % 64) * 8;
+    const unsigned long long t7 = clock64();
+    row[1] = t1; row[2] = t2; row[3] = t3; row[4] = t4; row[5] = t5; row[6] = t6; row[7] = t7;
+  }
+#endif
 }
 
-// Combine the update partials (one warp per value, fixed order) and, in the
-// last block to finish, record ||r||, test convergence, form beta and solve mu.
+// Combine the update partials and, in the last block to finish, record ||r||,
+// test convergence, form beta and solve mu. One block per reduced value: every
+// thread sums a fixed strided subset of the chunk partials, then a fixed-order
+// block reduction (deterministic, one L2 round trip instead of a serial walk).
+// Linv does not change during a run, so narrow factors are staged in shared
+// memory before waiting on the update kernel (overlapping its tail).
 __global__ void __launch_bounds__(256) k_pcg_finish(const rk_pcg_plan P, int entry, int64_t nchunks) {
   rk_pcg_state* st = P.st;
+  extern __shared__ double dyn[];      // Ls[w*w] (staged) | red[2 + m] | ysm[2 w]
+  __shared__ double scratch[32];
+  const int64_t m = P.m, w = P.wchol;
+  const int64_t nv = 2 + m;
+  const bool staged = w > 0 && w <= kStageFactor;
+  double* Ls = dyn;
+  double* red = dyn + (staged ? w * w : 0);
+  if (staged) {
+    for (int64_t e = threadIdx.x; e < w * w; e += blockDim.x) {
+      const int64_t col = e / w, row = e - col * w;
+      Ls[e] = row >= col ? P.L[row + col * P.ldl] : 0.0;
+    }
+  }
   pdl_wait();
   pdl_trigger();
   if (st->done) return;
-  extern __shared__ double dyn[];      // red[2 + m] | ysm[2 w] | Ls[w*w]
-  const int64_t m = P.m;
-  const int64_t nv = 2 + m;
   const double* part = P.partials;
   double* sums = P.partials + nv * nchunks;
-  const int lane = threadIdx.x & 31;
-  const int64_t v = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (v < nv) {
+  for (int64_t v = blockIdx.x; v < nv; v += gridDim.x) {
     const double* pv = part + v * nchunks;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;  // 4 independent chains, fixed order
-    int64_t b = lane;
-    for (; b + 96 < nchunks; b += 128) {
-      a0 += __ldcg(pv + b);
-      a1 += __ldcg(pv + b + 32);
-      a2 += __ldcg(pv + b + 64);
-      a3 += __ldcg(pv + b + 96);
-    }
-    for (; b < nchunks; b += 32) a0 += __ldcg(pv + b);
-    double a = warp_sum((a0 + a1) + (a2 + a3));
-    if (lane == 0) {
-      sums[v] = a;
-      __threadfence();  // publish before the block's ticket
-    }
+    double a[1] = {0.0};
+#pragma unroll 4
+    for (int64_t b = threadIdx.x; b < nchunks; b += blockDim.x) a[0] += __ldcg(pv + b);
+    block_sum<1>(a, scratch);
+    if (threadIdx.x == 0) sums[v] = a[0];
   }
-  if (!ticket_last(P.tickets + 1)) return;
+  if (!ticket_last(P.tickets + 1)) return;  // fences thread 0's sums before the ticket
   __threadfence();
-  double* red = dyn;
   for (int64_t j = threadIdx.x; j < nv; j += blockDim.x) red[j] = __ldcg(sums + j);
   __syncthreads();
-  const int64_t k = st->k;
-  __shared__ int s_stop;
-  if (threadIdx.x == 0) {
-    const double rr = red[0], rz_next = red[1];
-    const double rnorm = sqrt(rr);
-    st->rr = rr;
-    s_stop = 0;
-    if (entry) {
-      // krylov.py:268 history[0] = ||r0|| ; :292 rz = r @ z
-      P.res_h[0] = rnorm;
-      st->rz = rz_next;
-    } else {
-      P.res_h[k + 1] = rnorm;                  // krylov.py:314
-      if (rnorm <= st->threshold) {            // krylov.py:317
-        st->status = 1;
-        st->done = 1;
-        st->k = k + 1;
-        s_stop = 1;
-      } else {
-        st->rz_next = rz_next;                 // krylov.py:321
-        st->beta = rz_next / st->rz;           // krylov.py:324 (rz_next / rz)
-        st->rz = rz_next;                      // krylov.py:340
-      }
-    }
-  }
-  __syncthreads();
-  if (s_stop || m == 0) return;
-  double* ysm = red + nv;
-  solve_factor(P, red + 2, ysm, ysm + 2 * P.wchol, P.mu);
+  if (pcg_scalars(P, entry, red) || m == 0) return;
+  solve_factor(P, red + 2, red + nv, staged ? Ls : nullptr, P.mu);
 }
 
 // K5: new direction into V[:, k+1] (entry: V[:, 0]).
@@ -313,15 +475,18 @@ bool prof_sample();
 static int64_t update_chunks(int64_t n) { return std::max<int64_t>(1, (n + rk::kProjChunk - 1) / rk::kProjChunk); }
 
 static size_t finish_smem(int64_t m, int64_t wchol) {
-  return (size_t)(2 + m + 2 * wchol) * sizeof(double);
+  const int64_t staged = (wchol > 0 && wchol <= rk::kStageFactor) ? wchol * wchol : 0;
+  return (size_t)(staged + 2 + m + 2 * wchol) * sizeof(double);
 }
 
 int64_t pcg_workspace_doubles(int64_t n, int64_t m, int64_t vcap) {
   int64_t need = 0;
   // spmv / curvature partials: grid x 2
   need = std::max<int64_t>(need, (int64_t)sm_count() * 8 * 2);
-  // update partials (2 + m) x chunks, plus the (2 + m) sums
-  need = std::max<int64_t>(need, (2 + m) * (update_chunks(n) + 1));
+  // update partials (2 + m) x chunks, plus the (2 + m) sums or the
+  // (2 + m) x groups group sums of the fused finish
+  const int64_t nch = update_chunks(n);
+  need = std::max<int64_t>(need, (2 + m) * (nch + std::max<int64_t>(1, (nch + 31) / 32)));
   // fom gemv-t partials: chunks x vcap
   need = std::max<int64_t>(need, gemv_nchunks(n) * std::max<int64_t>(vcap, 1));
   return need;
@@ -357,13 +522,17 @@ static int check_plan(const rk_pcg_plan& P, bool need_proj) {
   return 0;
 }
 
-static void launch_update(const rk_pcg_plan& P, int entry, cudaStream_t s) {
+static int64_t fuse_group(int64_t nch) { return std::max<int64_t>(32, (nch + rk::kMaxGroups - 1) / rk::kMaxGroups); }
+
+static void launch_update(const rk_pcg_plan& P, int entry, cudaStream_t s, bool mark = false) {
   const int64_t nch = update_chunks(P.n);
   const int64_t groups = std::max<int64_t>(1, (P.m + rk::kProjCols - 1) / rk::kProjCols);
   dim3 grid((unsigned)nch, (unsigned)groups);
-  launch_pdl(rk::k_pcg_update, grid, dim3(rk::kUpdThreads), 0, s, P, entry);
-  const int64_t nv = 2 + P.m;
-  const unsigned fgrid = (unsigned)((nv + 7) / 8);
+  const int fused = P.m <= rk::kFuseMax ? 1 : 0;
+  launch_pdl(rk::k_pcg_update, grid, dim3(rk::kUpdThreads), 0, s, P, entry, fused, fuse_group(nch));
+  if (mark) prof_mark(2, s);
+  if (fused) return;
+  const unsigned fgrid = (unsigned)std::min<int64_t>(2 + P.m, 4096);
   launch_pdl(rk::k_pcg_finish, dim3(fgrid), dim3(256), finish_smem(P.m, P.wchol), s, P, entry, nch);
 }
 
@@ -380,6 +549,14 @@ static void launch_direction(const rk_pcg_plan& P, int entry, int64_t kmax, cuda
       launch_gemv_n(P.n, kmax, kk, done, P.V, P.ldv, P.coef, P.V, P.V, 2, 1, P.ldv, s);
     }
   }
+}
+
+int debug_trace(unsigned long long* out, int64_t n) {
+  const int64_t cnt = std::min<int64_t>(n, 64 * 8);
+  if (cnt <= 0) return 0;
+  if (cudaMemcpyFromSymbol(out, rk::g_tail_trace, cnt * sizeof(unsigned long long)) != cudaSuccess)
+    return cuda_check("rk_debug_trace");
+  return 0;
 }
 
 int pcg_entry(const rk_pcg_plan& P, cudaStream_t s) {
@@ -403,10 +580,10 @@ int pcg_steps(const rk_pcg_plan& P, int nsteps, int64_t kmax_hint, cudaStream_t 
     if (mark) prof_mark(0, s);
     launch_spmv_pcg(P, s);
     if (mark) prof_mark(1, s);
-    launch_update(P, 0, s);
-    if (mark) prof_mark(2, s);
-    launch_direction(P, 0, kmax_hint + 1, s);
+    launch_update(P, 0, s, mark);
     if (mark) prof_mark(3, s);
+    launch_direction(P, 0, kmax_hint + 1, s);
+    if (mark) prof_mark(4, s);
   }
   return cuda_check("rk_pcg_steps");
 }

@@ -13,6 +13,8 @@
 // (evict-first) so the gathered vector stays resident in L2.
 #include <algorithm>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace rk {
@@ -273,13 +275,14 @@ __global__ void __launch_bounds__(256) k_csr_asymmetry(int64_t n, const int32_t*
 }
 
 // ---------------------------------------------------------------------------
-// 3x3-block SpMV in sliced-ELL form (SELL-32 of 3x3 blocks, structure-of-
-// arrays values) for vector-valued problems such as the Q1 elasticity
-// operator. A warp owns a slice of 32 block rows, one block row (3 matrix rows)
-// per lane; slot t of the slice is read by all 32 lanes at once, so every load
-// of the block column and of each of the 9 values is a fully coalesced 128- or
-// 256-byte warp access, and the 3 consecutive x entries of the block column
-// are gathered per lane. 76 bytes per stored block (vs 108 for the same 9
+// 3x3-block SpMV in sliced-ELL form (SELL-32 of 3x3 blocks) for vector-valued
+// problems such as the Q1 elasticity operator. A warp owns a slice of 32 block
+// rows, one block row (3 matrix rows) per lane; slot t of the slice is read by
+// all 32 lanes at once, so every load of the block column and of each of the 9
+// values is a fully coalesced 128- or 256-byte warp access, the 9 value planes
+// of a slot row are one contiguous 2304-byte tile (one DRAM stream per warp
+// step), and the 3 consecutive x entries of the block column are gathered per
+// lane. 76 bytes per stored block (vs 108 for the same 9
 // nonzeros in CSR); slices are padded only to their widest row.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void sell3_row(const rk_csr& A, const double* __restrict__ x, int64_t slice, int lane,
@@ -287,17 +290,17 @@ __device__ __forceinline__ void sell3_row(const rk_csr& A, const double* __restr
   s0 = s1 = s2 = 0.0;
   const int32_t base = __ldg(A.browptr + slice);
   const int32_t width = (__ldg(A.browptr + slice + 1) - base) >> 5;
-  const int64_t ns = A.nblk;
   const int32_t* __restrict__ col = A.bcol + base + lane;
-  const double* __restrict__ val = A.bval + base + lane;
+  // slot row t of the slice: 9 x 32 values, contiguous (entry e at 32 e + lane)
+  const double* __restrict__ val = A.bval + 9 * (int64_t)base + lane;
   int32_t t = 0;
   for (; t + 2 <= width; t += 2) {  // two slots in flight per lane
     const int32_t ca = __ldcs(col + 32 * t), cb = __ldcs(col + 32 * (t + 1));
     double va[9], vb[9];
 #pragma unroll
     for (int e = 0; e < 9; ++e) {
-      va[e] = __ldcs(val + e * ns + 32 * t);
-      vb[e] = __ldcs(val + e * ns + 32 * (t + 1));
+      va[e] = __ldcs(val + 288 * t + 32 * e);
+      vb[e] = __ldcs(val + 288 * (t + 1) + 32 * e);
     }
     const double* xa = x + 3 * (int64_t)ca;
     const double* xb = x + 3 * (int64_t)cb;
@@ -314,7 +317,7 @@ __device__ __forceinline__ void sell3_row(const rk_csr& A, const double* __restr
     const int32_t ca = __ldcs(col + 32 * t);
     double va[9];
 #pragma unroll
-    for (int e = 0; e < 9; ++e) va[e] = __ldcs(val + e * ns + 32 * t);
+    for (int e = 0; e < 9; ++e) va[e] = __ldcs(val + 288 * t + 32 * e);
     const double* xa = x + 3 * (int64_t)ca;
     const double a0 = __ldg(xa), a1 = __ldg(xa + 1), a2 = __ldg(xa + 2);
     s0 = fma(va[0], a0, s0); s0 = fma(va[1], a1, s0); s0 = fma(va[2], a2, s0);
@@ -396,6 +399,15 @@ __global__ void k_bsr3_gather(int64_t total, const int32_t* __restrict__ perm, c
 // ---------------------------------------------------------------------------
 namespace rkh {
 
+static int spmv_blocks_per_sm() {
+  static const int v = [] {
+    const char* e = getenv("RK_SPMV_BPS");
+    const int x = e ? atoi(e) : 4;
+    return x > 0 ? x : 4;
+  }();
+  return v;
+}
+
 static int resident_blocks(const void* kern, int threads) {
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, 0) != cudaSuccess || occ < 1) occ = 1;
@@ -411,7 +423,10 @@ static int launch_bsr3_spmv(const rk_csr& A, const double* x, double* y, cudaStr
 }
 
 static void launch_bsr3_spmv_pcg(const rk_pcg_plan& P, cudaStream_t s) {
-  static const int cap = std::min(resident_blocks((const void*)rk::k_bsr3_spmv_pcg, rk::kSpmvThreads), sm_count() * 8);
+  // a fixed number of blocks per SM (when resident), so the order of the
+  // p'Ap / p'p partial sums does not follow register allocation
+  static const int cap = std::min(resident_blocks((const void*)rk::k_bsr3_spmv_pcg, rk::kSpmvThreads),
+                                  sm_count() * spmv_blocks_per_sm());
   const int64_t need = ((P.n / 3 + 31) / 32 + rk::kSpmvThreads / 32 - 1) / (rk::kSpmvThreads / 32);
   launch_pdl(rk::k_bsr3_spmv_pcg, dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(cap, need))),
              dim3(rk::kSpmvThreads), 0, s, P);

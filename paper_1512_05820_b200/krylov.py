@@ -274,7 +274,7 @@ class _Run:
         self.z = torch.empty(n, dtype=F64, device=device)
         self.mu = torch.zeros(max(m, 1), dtype=F64, device=device)
         self.st = torch.zeros(nat.STATE_BYTES, dtype=torch.uint8, device=device)
-        self.tickets = torch.zeros(16, dtype=torch.int32, device=device)
+        self.tickets = torch.zeros(nat.PCG_TICKETS, dtype=torch.int32, device=device)
         self.st_host = torch.empty(nat.STATE_BYTES, dtype=torch.uint8, pin_memory=True)
         self.cstate = nat.RkPcgState.from_buffer(self.st_host.numpy())
         self.vcap = 0

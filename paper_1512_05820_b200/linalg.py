@@ -197,7 +197,7 @@ SELL_SLICE = 32  # block rows per slice (one warp, one block row per lane)
 class _Bsr3:
     """Sliced-ELL view of a 3x3-block pattern (SELL-32 of 3x3 blocks): slice
     offsets (in slots), the block column of every slot and the permutation that
-    gathers CSR values into structure-of-arrays slot values (-1 = padding).
+    gathers CSR values into the slot-row value tiles (-1 = padding).
     ``nblk`` is the number of slots (real blocks + padding)."""
 
     def __init__(self, browptr, bcol, perm, nblk, nreal):
@@ -252,10 +252,13 @@ def _bsr3_from_host(rp: np.ndarray, ci: np.ndarray, n: int, device) -> _Bsr3 | N
     pos = np.arange(nslot, dtype=np.int64) - sptr[sl_of]
     scol[:] = np.minimum(sl_of * SELL_SLICE + pos % SELL_SLICE, nbr - 1)
     scol[slot] = bcol
+    # values: per slot row (32 lanes) a contiguous 9 x 32 tile, entry e of slot s
+    # at 9 * (s - s % 32) + 32 e + s % 32 (one 2304-byte stream per warp step)
     perm = np.full(9 * nslot, -1, dtype=np.int64)
+    tile = 9 * (slot - slot % SELL_SLICE) + slot % SELL_SLICE
     for a in range(3):
         for c in range(3):
-            perm[(3 * a + c) * nslot + slot] = first[a] + 3 * t_loc + c
+            perm[tile + SELL_SLICE * (3 * a + c)] = first[a] + 3 * t_loc + c
     to = lambda arr: torch.from_numpy(np.ascontiguousarray(arr, dtype=np.int32)).to(device)  # noqa: E731
     return _Bsr3(to(sptr), to(scol), to(perm), nslot, nblk)
 

@@ -51,19 +51,19 @@ t = time.time()
 xs, reps, _ = pk.run_sequence(dseq, cfg, precond_factory=lambda A: pk.build_preconditioner("jacobi", A))
 torch.cuda.synchronize()
 out["seq_s"] = time.time() - t
-ms = (ctypes.c_double * 3)()
-cnt = (ctypes.c_int64 * 3)()
+ms = (ctypes.c_double * 4)()
+cnt = (ctypes.c_int64 * 4)()
 lib.rk_profile_end(ms, cnt)
 out["reports"] = [dict(iters=r.stage3_iters, wall=r.wall_time, matvecs=r.matvecs, trunc=r.truncated,
                        res=r.final_residual) for r in reps]
 A = dspecs[0].A
 spmv_bytes = 12 * A.nnz + 4 * (A.n + 1) + 16 * A.n
-avg = [ms[i] / max(cnt[i], 1) for i in range(3)]
+avg = [ms[i] / max(cnt[i], 1) for i in range(4)]
 out["kernel_avg_ms"] = avg
 out["kernel_counts"] = list(cnt)
 out["spmv_GBps"] = spmv_bytes / (avg[0] * 1e-3) / 1e9
 out["update_GBps(m=60)"] = (64 * A.n + 60 * 8 * A.n) / (avg[1] * 1e-3) / 1e9
-out["direction_GBps(m=60)"] = (3 * 8 * A.n + 60 * 8 * A.n) / (avg[2] * 1e-3) / 1e9
+out["direction_GBps(m=60)"] = (3 * 8 * A.n + 60 * 8 * A.n) / (avg[3] * 1e-3) / 1e9
 
 if args.no_micro:
     print(json.dumps(out, indent=1))

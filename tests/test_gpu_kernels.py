@@ -68,6 +68,62 @@ def test_bsr3_view_for_vector_problems(pk):
     assert B.bval is None
 
 
+def _fma_chain_rows(H, x, rows):
+    """Exact emulation of the SELL kernel's arithmetic for the given matrix rows:
+    per stored 3x3 block in CSR order, s = fma(v_c, x_c, s) for c = 0, 1, 2
+    (rounded once per fma, via exact rationals)."""
+    from fractions import Fraction
+
+    out = []
+    for i in rows:
+        s = 0.0
+        lo, hi = int(H.row_offsets[i]), int(H.row_offsets[i + 1])
+        for q in range(lo, hi):
+            s = float(Fraction(float(H.values[q])) * Fraction(float(x[H.col_indices[q]])) + Fraction(s))
+        out.append(s)
+    return np.array(out)
+
+
+def test_sell_spmv_is_the_documented_fma_chain(pk):
+    """Bitwise: the 3x3-block SpMV (tiled slot-row layout) computes each row as
+    one fma chain over its blocks in CSR order, padding slots contributing
+    exactly nothing; the fused PCG SpMV uses the same row routine."""
+    from paper_1512_05820_b200.problems import elasticity_sequence
+
+    H = next(iter(elasticity_sequence((6, 5, 4), p=1))).A
+    A = pk.SparseSpdMatrix(H.n, H.row_offsets, H.col_indices, H.values)
+    assert A.bval is not None
+    x = np.random.default_rng(17).standard_normal(H.n)
+    got = pk.spmv(A, x).cpu().numpy()
+    rows = np.arange(H.n)
+    assert np.array_equal(got, _fma_chain_rows(H, x, rows))
+
+
+def test_sell_spmv_fma_chain_at_c3_size(pk):
+    """The same bitwise check on sampled rows of the full C3 matrix (64^3 Q1
+    elasticity, 811,200 rows), for the plain and the fused PCG SpMV."""
+    from paper_1512_05820_b200.problems import elasticity_sequence
+
+    H = next(iter(elasticity_sequence((64, 64, 64), p=1))).A
+    A = pk.SparseSpdMatrix(H.n, H.row_offsets, H.col_indices, H.values)
+    assert A.bval is not None
+    x = np.random.default_rng(23).standard_normal(H.n)
+    rows = np.unique(np.concatenate([np.arange(96), H.n - 1 - np.arange(96),
+                                     np.random.default_rng(5).integers(0, H.n, 1500)]))
+    want = _fma_chain_rows(H, x, rows)
+    got = pk.spmv(A, x).cpu().numpy()
+    assert np.array_equal(got[rows], want)
+    # fused: one stepped PCG iteration stores A p_0 with p_0 = z = D^{-1} b
+    M = pk.build_preconditioner("jacobi", A)
+    b = torch.from_numpy(x).cuda()
+    try:
+        res = pk.augmented_pcg(A, b, precond=M, tol=0.0, max_iter=1, keep_products=True)
+    except pk.NotConverged as exc:
+        res = exc.partial
+    p0 = res.V[:, 0].cpu().numpy()  # V holds the directions p_k as iterated
+    assert np.array_equal(res.AV[:, 0].cpu().numpy()[rows], _fma_chain_rows(H, p0, rows))
+
+
 def test_spmv_sink_counts_one_matvec(pk):
     A = pk.SparseSpdMatrix.identity(5)
     sink = pk.InstrumentationSink()

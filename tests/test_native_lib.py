@@ -39,13 +39,14 @@ def test_struct_layouts_match_c(tmp_path):
 
     src = tmp_path / "sz.c"
     src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "podcg.h"\n'
-                   'int main(){printf("%zu %zu %zu %zu %zu\\n", sizeof(rk_pcg_plan), sizeof(rk_pcg_state),'
-                   ' sizeof(rk_csr), offsetof(rk_pcg_plan, mode), offsetof(rk_pcg_plan, st));return 0;}\n')
+                   'int main(){printf("%zu %zu %zu %zu %zu %d\\n", sizeof(rk_pcg_plan), sizeof(rk_pcg_state),'
+                   ' sizeof(rk_csr), offsetof(rk_pcg_plan, mode), offsetof(rk_pcg_plan, st), RK_PCG_TICKETS);'
+                   'return 0;}\n')
     exe = tmp_path / "sz"
     subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()
     got = [ctypes.sizeof(_native.RkPcgPlan), ctypes.sizeof(_native.RkPcgState), ctypes.sizeof(_native.RkCsr),
-           _native.RkPcgPlan.mode.offset, _native.RkPcgPlan.st.offset]
+           _native.RkPcgPlan.mode.offset, _native.RkPcgPlan.st.offset, _native.PCG_TICKETS]
     assert list(map(int, out)) == got
 
 
