@@ -165,6 +165,14 @@ int rk_spmm(const rk_csr* A, int64_t m, const double* X, int64_t ldx, double* Y,
  * (preconditioners.py:54-58, linalg.py:114-119). */
 int rk_csr_diagonal(const rk_csr* A, double* diag, double* dinv, int64_t* bad_row,
                     void* stream);
+/* SSOR application z = M^{-1} r, M = (D/w + L) D^{-1} (D/w + L)' with A = L + D + L'
+ * (preconditioners.py:64-90): forward sweep over A's lower triangle into work
+ * (n doubles), then the backward sweep over its upper triangle with rhs work * d.
+ * dw = fl(d / w), d = diag(A). Sync-free triangular solves: flags (2n int32,
+ * zero-initialised once) are compared against epoch, which the caller increases
+ * with every application; counters: 2 uint32 (reset by the call). */
+int rk_ssor_apply(const rk_csr* A, const double* dw, const double* d, const double* r, double* z, double* work,
+                  int32_t* flags, uint32_t* counters, int32_t epoch, void* stream);
 /* bval[s] = perm[s] >= 0 ? val[perm[s]] : 0 for s < 9*nblk: refresh the
  * 3x3-block slot values of a matrix whose pattern (and perm) was built once
  * for the sequence. */

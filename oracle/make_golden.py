@@ -6,6 +6,7 @@ fixtures to tests/golden/. The GPU box never reads /root/reference: the tests
 there only read these committed fixtures.
 
     python oracle/make_golden.py            # rewrites tests/golden/*.npz
+    python oracle/make_golden.py run_next_strategies   # one generator only
 """
 
 from __future__ import annotations
@@ -304,18 +305,67 @@ def run_kernels(rk):
     return {"kernels": out}
 
 
+NEXT_CASES = {
+    "ctcr_": (dict(strategy="pod-ctc-rbf", nu_y=1.0, nu_w=1.0, storage_cap=25, max_dim=10), "cg", "jacobi"),
+    "ctcp_": (dict(strategy="pod-ctc-prev", nu_y=0.999, nu_w=0.9, storage_cap=25, max_dim=10), "fom", "jacobi"),
+    "defl_": (dict(strategy="deflate", deflate_dim=8, storage_cap=25), "cg", "jacobi"),
+    "defs_": (dict(strategy="deflate", deflate_dim=8, stage1_dim=4, storage_cap=25), "fom", "jacobi"),
+    "ssor_": (dict(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=20, max_dim=12), "cg", "ssor"),
+    "ssor15_": (dict(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=20, max_dim=12), "fom", "ssor:1.5"),
+}
+
+
+def run_next_strategies(rk):
+    """SURVEY 8f f3/f4 through the reference: output-metric POD (pod-ctc-*, with
+    the A-orthonormalisation), harmonic-Ritz deflation and SSOR preconditioning
+    on a drifting diffusion sequence with a 2-row output matrix; plus kernel-level
+    vectors for pod_svd, deflation_compress and one SSOR application."""
+    from recykl import preconditioners
+    from recykl.linalg import SparseSpdMatrix
+    from recykl.pod import pod_svd
+    from recykl.problems import gen_diffusion_sequence, gen_output_matrix
+    from recykl.threestage import SolverConfig, run_sequence
+    from recykl.truncation import TruncationConfig, deflation_compress
+
+    seq = gen_diffusion_sequence((10, 10), p=6, delta=0.05, seed=41, tol=1e-9)
+    seq.C = gen_output_matrix(2, seq.n, seed=3)
+    d = _pack_sequence(seq, "")
+    d["C"] = seq.C
+    for tag, (tr, mode, pc) in NEXT_CASES.items():
+        kind, omega = (pc.split(":") + ["1.0"])[:2] if pc.startswith("ssor") else (pc, "1.0")
+        pf = lambda A, kind=kind, omega=float(omega): preconditioners.build(kind, A, omega)  # noqa: E731
+        cfg = SolverConfig(truncation=TruncationConfig(**tr), mode=mode)
+        xs, reps, _ = run_sequence(seq, cfg, precond_factory=pf)
+        d.update(_pack_run(xs, reps, tag))
+        for j, x in enumerate(xs, start=1):
+            d[f"{tag}q{j}"] = seq.C @ x
+    # kernel level
+    rng = np.random.default_rng(11)
+    A = seq[0].A
+    S = rng.standard_normal((seq.n, 14))
+    gam = rng.uniform(0.5, 2.0, 14)
+    r = pod_svd(S, gam, seq.C, 1.0)
+    d["k_S"], d["k_gamma"] = S, gam
+    d["k_svd_sigma"], d["k_svd_y"], d["k_svd_cols"] = r.singular_values, np.int64(r.y), r.columns
+    out = deflation_compress(S, A, 6, stage1_dim=None)
+    d["k_defl_Y"], d["k_defl_mu"], d["k_defl_map"] = out.Y_new, out.spectrum, out.truncation_map
+    M = preconditioners.build("ssor", A, 1.3)
+    v = rng.standard_normal(seq.n)
+    d["k_ssor_r"], d["k_ssor_z"] = v, M.apply(v)
+    assert isinstance(A, SparseSpdMatrix)
+    return {"next_strategies": d}
+
+
 def main():
     rk = _ref()
     os.makedirs(OUT, exist_ok=True)
     blobs = {}
-    blobs.update(run_fixture_cases(rk))
-    blobs.update(run_stage_variants(rk))
-    blobs.update(run_kernels(rk))
-    blobs.update(run_elasticity(rk))
-    blobs.update(run_c1(rk))
-    blobs.update(run_c2_small(rk))
-    blobs.update(run_c3_mid(rk))
-    blobs.update(run_c5_small(rk))
+    only = sys.argv[1:]
+    runs = [run_fixture_cases, run_stage_variants, run_kernels, run_elasticity, run_c1, run_c2_small, run_c3_mid,
+            run_c5_small, run_next_strategies]
+    for fn in runs:
+        if not only or fn.__name__ in only:
+            blobs.update(fn(rk))
     for name, d in blobs.items():
         path = os.path.join(OUT, f"{name}.npz")
         np.savez_compressed(path, **d)

@@ -162,8 +162,9 @@ def aug_pcg(apply, b, yhat0=None, Y=None, proj=None, dinv=None, tol=0.0, *, mode
             identity_precond=False):
     """Restatement of augmented_pcg (krylov.py:181-345).
 
-    ``apply`` charges its own matvecs; ``dinv`` is the Jacobi inverse diagonal
-    (None: no preconditioner, or the identity when ``identity_precond``).
+    ``apply`` charges its own matvecs; ``dinv`` is the Jacobi inverse diagonal or
+    a callable preconditioner (None: no preconditioner, or the identity when
+    ``identity_precond``).
     """
     b = np.asarray(b, dtype=np.float64)
     n = b.shape[0]
@@ -172,6 +173,8 @@ def aug_pcg(apply, b, yhat0=None, Y=None, proj=None, dinv=None, tol=0.0, *, mode
     def precondition(r):
         if has_pc and tally is not None:
             tally.precond += 1
+        if callable(dinv):
+            return dinv(r)
         return r * dinv if dinv is not None else r.copy()
 
     if Y is not None and Y.shape[1] == 0:
@@ -309,6 +312,63 @@ def prev_weights(history):
     return out
 
 
+def pod_svd(S, gamma, chalf, eps):
+    """pod.py:134-157: thin SVD of chalf (S gamma), zero-padded spectrum."""
+    factored = np.atleast_2d(chalf) @ (S * gamma)
+    _, sigma, Vt = np.linalg.svd(factored, full_matrices=False)
+    V = Vt.T
+    s = S.shape[1]
+    if sigma.shape[0] < s:
+        sigma = np.concatenate([sigma, np.zeros(s - sigma.shape[0])])
+        Vf = np.zeros((s, s))
+        Vf[:, : V.shape[1]] = V
+        V = Vf
+    y = energy_dim(sigma**2, eps)
+    coef = (V[:, :y] / sigma[:y]) * gamma[:, None]
+    return S @ coef, sigma, y, coef
+
+
+def enforce_a_orth(Y, A, tally):
+    """truncation.py:191-206: Y L^{-T} with Y'AY = L L'."""
+    G, _ = gram_with_product(A, Y, tally)
+    L = cholesky_lower(0.5 * (G + G.T))
+    return scipy.linalg.solve_triangular(L, Y.T, lower=True).T, L
+
+
+def deflation(Z, A, m, stage1_dim, tally):
+    """truncation.py:152-188 (linalg.py:293-307 for the generalized EVD)."""
+    m = min(int(m), Z.shape[1])
+    G, AZ = gram_with_product(A, Z, tally)
+    K = AZ.T @ AZ
+    w, V = scipy.linalg.eigh(0.5 * (K + K.T), 0.5 * (G + G.T))
+    keep = V[:, :m]  # the m smallest harmonic Ritz values (scipy's order is ascending)
+    Y = Z @ keep
+    gy = keep.T @ G @ keep
+    L = cholesky_lower(0.5 * (gy + gy.T))
+    Yo = scipy.linalg.solve_triangular(L, Y.T, lower=True).T
+    return Yo, (m if stage1_dim is None else min(stage1_dim, m)), w[:m]
+
+
+class Ssor:
+    """preconditioners.py:64-90: M = (D/w + L) D^{-1} (D/w + L)', z = M^{-1} r by
+    a forward and a backward triangular sweep."""
+
+    def __init__(self, A, omega=1.0):
+        A = as_csr(A)
+        d = A.diagonal()
+        self.d = d
+        low = scipy.sparse.tril(A, k=-1) + scipy.sparse.diags(d / omega)
+        self.low = scipy.sparse.csr_matrix(low)
+        self.up = scipy.sparse.csr_matrix(low.T)
+
+    def __call__(self, r):
+        import scipy.sparse.linalg as spla
+
+        u = spla.spsolve_triangular(self.low, r, lower=True)
+        u = u * self.d
+        return spla.spsolve_triangular(self.up, u, lower=False)
+
+
 @dataclass
 class Config:
     """SolverConfig + TruncationConfig fields the hot path reads
@@ -326,6 +386,7 @@ class Config:
     recycle: bool = True
     max_iter: int | None = None
     rbf_window: int | None = None
+    deflate_dim: int | None = None
 
 
 def _cap(v, pin, hard):
@@ -400,7 +461,7 @@ class InnerProjection:
 
 
 def solve_one(A, b, xbar, state: State, eps, cfg: Config, dinv=None, identity_precond=False, eps_hat=None,
-              eps_inner=None):
+              eps_inner=None, chalf=None):
     """threestage.py:230-452 (solve_system) + 455-547 (update_basis)."""
     A = as_csr(A)
     tally = Tally()
@@ -479,14 +540,15 @@ def solve_one(A, b, xbar, state: State, eps, cfg: Config, dinv=None, identity_pr
     rep.stage3_iters = res3.k
     rep.final_residual = float(res3.history[-1])
     rep.stage3_basis = basis3
-    _fold(state, yhat, res3, cfg, A, tally, stage1_gram, rep)
+    _fold(state, yhat, res3, cfg, A, tally, stage1_gram, rep, chalf=chalf)
     rep.matvecs, rep.precond_applies = tally.matvecs, tally.precond
     rep.wall_time = time.perf_counter() - t0
     return x, rep
 
 
-def _fold(state: State, yhat, res3: PcgOut, cfg: Config, A, tally, stage1_gram, rep):
-    """update_basis (threestage.py:455-547) for the pod-a-* and none strategies."""
+def _fold(state: State, yhat, res3: PcgOut, cfg: Config, A, tally, stage1_gram, rep, chalf=None):
+    """update_basis (threestage.py:455-547) with compress (truncation.py:209-257):
+    pod-a-*, pod-ctc-* (then A-orthonormalised), deflate and none."""
     j = state.seen + 1
     if not cfg.recycle:
         state.seen = j
@@ -510,23 +572,33 @@ def _fold(state: State, yhat, res3: PcgOut, cfg: Config, A, tally, stage1_gram, 
     if eta.size:
         state.history.append(eta.copy())
     if Z.shape[1] > cfg.storage_cap and cfg.strategy != "none":
-        if cfg.strategy not in ("pod-a-rbf", "pod-a-prev"):
-            raise NotImplementedError(cfg.strategy)
+        if cfg.strategy == "deflate":
+            basis, wk, mu = deflation(Z, A, cfg.deflate_dim, cfg.stage1_dim, tally)
+            state.history.clear()
+            state.Y, state.idx, state.last_trunc = basis, list(range(wk)), j
+            rep.truncated, rep.spectrum = True, mu
+            state.seen = j
+            return
         if cfg.strategy.endswith("prev"):
             gam = prev_weights(state.history)
         else:
             window = cfg.rbf_window if cfg.rbf_window is not None else len(state.history)
             gam = rbf_weights(state.history, window)
-        if stage1_gram is not None and cfg.mode == "fom" and k > 0:
-            y_old = state.Y.shape[1]
-            G = np.zeros((y_old + k, y_old + k))
-            G[:y_old, :y_old] = stage1_gram
-            G[y_old:, y_old:] = np.eye(k)
+        if cfg.strategy.startswith("pod-ctc"):
+            basis, sigma, ycrit, coef = pod_svd(Z, gam, chalf, cfg.nu_y)
         else:
-            G, _ = gram_with_product(A, Z, tally)
-        basis, sigma, ycrit, coef = pod_from_gram(G, Z, gam, cfg.nu_y)
+            if stage1_gram is not None and cfg.mode == "fom" and k > 0:
+                y_old = state.Y.shape[1]
+                G = np.zeros((y_old + k, y_old + k))
+                G[:y_old, :y_old] = stage1_gram
+                G[y_old:, y_old:] = np.eye(k)
+            else:
+                G, _ = gram_with_product(A, Z, tally)
+            basis, sigma, ycrit, coef = pod_from_gram(G, Z, gam, cfg.nu_y)
         yk = _cap(ycrit, cfg.max_dim, ycrit)
         wk = _cap(energy_dim(sigma ** 2, cfg.nu_w), cfg.stage1_dim, yk)
+        if cfg.strategy.startswith("pod-ctc"):
+            basis, _ = enforce_a_orth(basis[:, :yk], A, tally)
         state.history.clear()
         state.Y = basis[:, :yk]
         state.idx = list(range(wk))
@@ -540,7 +612,8 @@ def _fold(state: State, yhat, res3: PcgOut, cfg: Config, A, tally, stage1_gram, 
 
 
 def run_sequence(seq, cfg: Config, precond: str | None = "jacobi", *, max_systems=None, keep=False):
-    """threestage.py:550-596 with a Jacobi (or no / identity) preconditioner per system.
+    """threestage.py:550-596 with a Jacobi, SSOR ("ssor" / "ssor:<omega>",
+    preconditioners.py:64-104) or no / identity preconditioner per system.
 
     Returns (solutions, reports, bases) where bases[j] is the basis after system j
     when ``keep``."""
@@ -552,9 +625,14 @@ def run_sequence(seq, cfg: Config, precond: str | None = "jacobi", *, max_system
         A = as_csr(spec.A)
         if state is None:
             state = State(n=A.shape[0], Y=np.zeros((A.shape[0], 0)))
-        dinv = 1.0 / A.diagonal() if precond == "jacobi" else None
+        if precond == "jacobi":
+            dinv = 1.0 / A.diagonal()
+        elif precond is not None and precond.startswith("ssor"):
+            dinv = Ssor(A, float(precond.split(":")[1]) if ":" in precond else 1.0)
+        else:
+            dinv = None
         x, rep = solve_one(A, spec.b, spec.xbar, state, spec.tol, cfg, dinv=dinv,
-                           identity_precond=(precond == "identity"))
+                           identity_precond=(precond == "identity"), chalf=getattr(seq, "C", None))
         xs.append(x)
         reps.append(rep)
         if keep:

@@ -133,6 +133,7 @@ _SIGNATURES = {
     "rk_profile_begin": (c_i32, []),
     "rk_launch_count": (c_i64, []),
     "rk_debug_trace": (c_i32, [ctypes.POINTER(ctypes.c_uint64), c_i64]),
+    "rk_ssor_apply": (c_i32, [ctypes.POINTER(RkCsr), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp]),
     "rk_profile_end": (c_i32, [ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64)]),
 }
 

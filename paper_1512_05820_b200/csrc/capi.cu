@@ -90,6 +90,8 @@ int launch_spmv(const rk_csr& A, const double* x, double* y, cudaStream_t s);
 int launch_spmm(const rk_csr& A, int64_t m, const double* X, int64_t ldx, double* Y, int64_t ldy, cudaStream_t s);
 int launch_csr_diagonal(const rk_csr& A, double* diag, double* dinv, int64_t* bad, cudaStream_t s);
 int launch_csr_asymmetry(const rk_csr& A, double* out2, double* ws, int64_t ws_len, uint32_t* tickets, cudaStream_t s);
+int launch_ssor_apply(const rk_csr& A, const double* dw, const double* d, const double* r, double* z, double* u,
+                      int* flags, unsigned int* counters, int epoch, cudaStream_t s);
 int pcg_entry(const rk_pcg_plan& P, cudaStream_t s);
 int pcg_steps(const rk_pcg_plan& P, int nsteps, int64_t kmax_hint, cudaStream_t s);
 int pcg_curvature(const rk_pcg_plan& P, cudaStream_t s);
@@ -207,6 +209,15 @@ int rk_csr_diagonal(const rk_csr* A, double* diag, double* dinv, int64_t* bad_ro
   if (int e = rkh::check_csr(A)) return e;
   RK_REQUIRE(bad_row, RK_ERR_ARG, "rk_csr_diagonal: null bad_row");
   return rkh::launch_csr_diagonal(*A, diag, dinv, bad_row, as_stream(stream));
+}
+
+int rk_ssor_apply(const rk_csr* A, const double* dw, const double* d, const double* r, double* z, double* work,
+                  int32_t* flags, uint32_t* counters, int32_t epoch, void* stream) {
+  if (int e = rkh::check_csr(A)) return e;
+  RK_REQUIRE(A->n == 0 || (dw && d && r && z && work && flags && counters), RK_ERR_ARG, "rk_ssor_apply: null pointer");
+  RK_REQUIRE(epoch > 0, RK_ERR_ARG, "rk_ssor_apply: epoch must be positive");
+  return rkh::launch_ssor_apply(*A, dw, d, r, z, work, reinterpret_cast<int*>(flags),
+                                reinterpret_cast<unsigned int*>(counters), epoch, as_stream(stream));
 }
 
 int rk_bsr3_gather(int64_t nblk, const int32_t* perm, const double* val, double* bval, void* stream) {

@@ -41,6 +41,7 @@ from .linalg import (
     as_vector,
     block_ld,
     dense_cholesky,
+    dot,
     empty_block,
     gemv_n,
     gemv_t,
@@ -423,6 +424,12 @@ def augmented_pcg(
         if reduced_solver is None:
             reduced_solver = DirectReducedProjection.assemble(operator, Y)
 
+    if precond is not None and not isinstance(precond, (JacobiPreconditioner, IdentityPreconditioner)):
+        # a preconditioner without a fused form (SSOR): the reference loop,
+        # step by step, on device primitives
+        return _augmented_pcg_generic(operator, bd, Y, yh if Y is not None else None, reduced_solver, precond,
+                                      tol, mode, paper_fom_beta, relative, max_iter, sink, r0, monitor)
+
     code = _MODES.get(mode, -1)
     if code == 1 and paper_fom_beta:
         code = 2
@@ -503,6 +510,94 @@ def augmented_pcg(
         f"no convergence to {threshold:.3e} within {max_iter} iterations",
         partial=_result(run, max_iter, False),
     )
+
+
+def _augmented_pcg_generic(operator, bd, Y, yh, reduced_solver, precond, tol, mode, paper_fom_beta, relative,
+                           max_iter, sink, r0, monitor) -> AugmentedPcgResult:
+    """krylov.py:234-345 line by line for a preconditioner applied by its own
+    kernels (z = M^{-1} r between the residual update and the reductions):
+    SpMV, deterministic dots, numpy-rounded axpys, GEMV-T/N for the
+    projection; the scalars come to the host every iteration. The fom sweeps
+    are modified Gram-Schmidt as in the reference."""
+    from .linalg import axpby
+
+    n = int(operator.dim)
+    dev = operator.device
+    hval = lambda t: float(t.cpu())  # noqa: E731
+    x = gemv_n(Y, yh) if Y is not None else torch.zeros(n, dtype=torch.float64, device=dev)
+    if r0 is not None:
+        r = as_vector(r0, dev, copy=True)
+        if r.shape[0] != n:
+            raise DimensionMismatch("augmented_pcg: r0 length mismatch")
+    elif Y is not None and bool(torch.any(x != 0)):
+        r = bd - as_vector(operator.apply(x), dev)
+    else:
+        r = bd.clone()
+    threshold = tol * norm(bd) if relative else tol
+    history = [norm(r)]
+    if monitor is not None:
+        monitor(0, x.clone())
+
+    def result(k, alphas, dirs, gammas, converged):
+        V = torch.stack(dirs, dim=1) if dirs else torch.zeros((n, 0), dtype=torch.float64, device=dev)
+        res = AugmentedPcgResult(k=k, vhat=np.asarray(alphas, dtype=np.float64), V=as_block(V, dev),
+                                 gamma=np.asarray(gammas, dtype=np.float64),
+                                 residual_history=np.asarray(history), x=x, converged=converged)
+        res.AV = None
+        return res
+
+    if history[0] <= threshold:
+        return result(0, [], [], [], True)
+    if max_iter is None:
+        max_iter = n
+
+    def project(z):
+        mu = reduced_solver(z)
+        return gemv_n(Y, mu, z, op=2)  # z - Y mu
+
+    z = precond.apply(r, sink)
+    p = project(z) if Y is not None else z.clone()
+    rz = hval(dot(r, z))
+    alphas, dirs, gammas, a_dirs, rz_hist = [], [], [], [], []
+    for k in range(max_iter):
+        Ap = as_vector(operator.apply(p), dev)
+        gamma = hval(dot(p, Ap))
+        if not np.isfinite(gamma) or gamma <= _BREAKDOWN_RTOL * hval(dot(p, p)):
+            raise Breakdown(f"direction curvature {gamma:.3e} at iteration {k}")
+        alpha = rz / gamma
+        x = axpby(alpha, p, 1.0, x)
+        r = axpby(-alpha, Ap, 1.0, r)
+        alphas.append(alpha)
+        dirs.append(p)
+        gammas.append(gamma)
+        rz_hist.append(rz)
+        if mode == "fom":
+            a_dirs.append(Ap)
+        history.append(norm(r))
+        if monitor is not None:
+            monitor(k + 1, x.clone())
+        if history[-1] <= threshold:
+            return result(k + 1, alphas, dirs, gammas, True)
+        z = precond.apply(r, sink)
+        rz_next = hval(dot(r, z))
+        if mode == "cg":
+            p = axpby(1.0, z, rz_next / rz, p.clone())
+            if Y is not None:
+                p = gemv_n(Y, reduced_solver(z), p, op=2)
+        elif mode == "fom":
+            p = project(z) if Y is not None else z.clone()
+            if paper_fom_beta:
+                for i in range(len(dirs)):
+                    p = axpby(rz_next / rz_hist[i], dirs[i], 1.0, p)
+            else:
+                for _ in range(2):
+                    for i in range(len(dirs)):
+                        p = axpby(-(hval(dot(a_dirs[i], p)) / gammas[i]), dirs[i], 1.0, p)
+        else:
+            raise ValueError(f"unknown mode {mode!r}")
+        rz = rz_next
+    raise NotConverged(f"no convergence to {threshold:.3e} within {max_iter} iterations",
+                       partial=result(max_iter, alphas, dirs, gammas, False))
 
 
 def _count_matvecs(operator, count):

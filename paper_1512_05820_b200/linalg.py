@@ -619,6 +619,14 @@ def gemv_n(B: torch.Tensor, c, y0: torch.Tensor | None = None, op: int = 0,
     return out
 
 
+def axpby(a: float, x: torch.Tensor, b: float, y: torch.Tensor) -> torch.Tensor:
+    """y <- fl(fl(a x) + fl(b y)) in place (numpy's `y + a * x` when b = 1)."""
+    if y.numel():
+        nat.check(nat.lib().rk_axpby(int(y.numel()), float(a), x.data_ptr(), float(b), y.data_ptr(),
+                                     nat.stream_ptr(y.device)), "axpby")
+    return y
+
+
 def dot(x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
     """x'y as a 1-element device tensor (deterministic)."""
     dev = x.device
@@ -797,6 +805,21 @@ def symmetric_evd(G):
     except np.linalg.LinAlgError as exc:
         raise IterationLimit(f"symmetric EVD did not converge: {exc}") from exc
     return w[::-1].copy(), V[:, ::-1].copy()
+
+
+def generalized_symmetric_evd(K, Mmat):
+    """K G = Mmat G diag(w) for symmetric K and SPD Mmat (linalg.py:293-307):
+    host LAPACK (scipy eigh, dsygvd) on the small z x z pair, eigenvalues
+    descending, eigenvectors Mmat-orthonormal."""
+    K = np.asarray(_host(K), dtype=np.float64)
+    Mmat = np.asarray(_host(Mmat), dtype=np.float64)
+    if K.shape != Mmat.shape:
+        raise DimensionMismatch("generalized EVD: operand shapes differ")
+    try:
+        w, G = scipy.linalg.eigh(K, Mmat)
+    except (np.linalg.LinAlgError, scipy.linalg.LinAlgError) as exc:
+        raise NotPositiveDefinite(f"mass matrix is not SPD: {exc}") from exc
+    return w[::-1].copy(), G[:, ::-1].copy()
 
 
 def thin_svd(B):

@@ -27,7 +27,9 @@ from .linalg import (
     assemble_gram,
     block_ld,
     gemm_nn,
+    gram,
     symmetric_evd,
+    thin_svd,
     to_numpy,
 )
 
@@ -161,6 +163,36 @@ def _pod_device(gram_sts, Sd, gamma, eps, max_cols):
         y=y,
         snapshot_coef=coef_cm.cpu().numpy(),
     )
+
+
+def pod_svd(S, gamma, chalf, eps: float, *, max_cols: int | None = None) -> PodBasisResult:
+    """POD in the output metric Theta = F'F through the thin SVD of the factored
+    weighted snapshots F (S diag(gamma)) (pod.py:134-157).
+
+    F (``chalf``, q x N) usually has a handful of rows, so the N-sized
+    contraction F S is the DMMA Gram S' F' (s x q) on the device; the q x s SVD
+    runs in host LAPACK as in the reference, and the basis is the DMMA
+    reconstruction S @ coef. Components beyond the factor rank carry zero
+    energy (the spectrum is zero-padded to s)."""
+    Sd = as_block(S)
+    gamma = np.asarray(to_numpy(gamma), dtype=np.float64)
+    F = chalf.detach() if isinstance(chalf, torch.Tensor) else np.atleast_2d(np.asarray(chalf, dtype=np.float64))
+    if F.ndim == 1:
+        F = F[None, :]
+    if gamma.shape[0] != Sd.shape[1]:
+        raise DimensionMismatch("one weight per snapshot required")
+    if F.shape[1] != Sd.shape[0]:
+        raise DimensionMismatch("metric factor columns must match snapshot length")
+    Ft = as_block(F.t() if isinstance(F, torch.Tensor) else F.T, Sd.device)  # N x q
+    factored = to_numpy(gram(Ft, Sd)) * gamma[None, :]                    # q x s = F S diag(gamma)
+    _, sigma, V = thin_svd(factored)
+    s = Sd.shape[1]
+    if sigma.shape[0] < s:
+        sigma = np.concatenate([sigma, np.zeros(s - sigma.shape[0])])
+        Vfull = np.zeros((s, s))
+        Vfull[:, : V.shape[1]] = V
+        V = Vfull
+    return _finalize(Sd, gamma, sigma, V, eps, max_cols=max_cols)
 
 
 def pod_evd(S, gamma, theta, eps: float, *, max_cols: int | None = None) -> PodBasisResult:

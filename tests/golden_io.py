@@ -46,3 +46,21 @@ def counters(d, prefix):
 
 
 pattern_sequence = elasticity_sequence  # same layout: rowptr, col, val{j}, b{j}, tol{j}, c
+
+
+# SURVEY 8f f3/f4 cases (oracle/make_golden.py NEXT_CASES): truncation config,
+# mode, preconditioner
+NEXT_CASES = {
+    "ctcr_": (dict(strategy="pod-ctc-rbf", nu_y=1.0, nu_w=1.0, storage_cap=25, max_dim=10), "cg", "jacobi"),
+    "ctcp_": (dict(strategy="pod-ctc-prev", nu_y=0.999, nu_w=0.9, storage_cap=25, max_dim=10), "fom", "jacobi"),
+    "defl_": (dict(strategy="deflate", deflate_dim=8, storage_cap=25), "cg", "jacobi"),
+    "defs_": (dict(strategy="deflate", deflate_dim=8, stage1_dim=4, storage_cap=25), "fom", "jacobi"),
+    "ssor_": (dict(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=20, max_dim=12), "cg", "ssor"),
+    "ssor15_": (dict(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=20, max_dim=12), "fom", "ssor:1.5"),
+}
+
+
+def next_sequence(d):
+    seq = sequence(d)
+    seq.C = d["C"]
+    return seq

@@ -1,0 +1,102 @@
+"""SURVEY 8f f3/f4 on the device: output-metric POD (pod-ctc-*, thin SVD of C S
+plus the explicit A-orthonormalisation), harmonic-Ritz deflation and the SSOR
+preconditioner (sync-free triangular sweeps), against runs of the reference
+itself (tests/golden/next_strategies.npz) and the CPU oracle."""
+
+import numpy as np
+import pytest
+import torch
+
+import golden_io as gio
+from test_gpu_sequence import _check, _run
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pk():
+    import paper_1512_05820_b200 as pk
+
+    return pk
+
+
+def _same_up_to_sign(got, ref, tol):
+    for j in range(ref.shape[1]):
+        s = np.sign(got[:, j] @ ref[:, j])
+        assert np.linalg.norm(s * got[:, j] - ref[:, j]) <= tol * np.linalg.norm(ref[:, j]), j
+
+
+@pytest.mark.parametrize("tag", list(gio.NEXT_CASES))
+def test_next_strategy_sequences(pk, tag):
+    d = gio.load("next_strategies")
+    tr, mode, pc = gio.NEXT_CASES[tag]
+    seq = gio.next_sequence(d)
+    xs, reps, _ = _run(pk, seq, tr, mode, pc)
+    first = _check(d, tag, xs, reps, strict=False)
+    assert all(r.converged for r in reps)
+    assert [bool(r.truncated) for r in reps] == list(map(bool, d[f"{tag}truncated"]))
+    for j, x in enumerate(xs, start=1):
+        q = d["C"] @ x.cpu().numpy()
+        ref = d[f"{tag}q{j}"]
+        tol = 1e-10 if j - 1 < first else 1e-4
+        assert np.all(np.abs(q - ref) <= tol * np.abs(ref)), (tag, j)
+
+
+def test_pod_svd_matches_reference(pk):
+    d = gio.load("next_strategies")
+    res = pk.pod_svd(d["k_S"], d["k_gamma"], d["C"], 1.0)
+    sig = d["k_svd_sigma"]
+    np.testing.assert_allclose(res.singular_values, sig, rtol=1e-12, atol=1e-13 * sig[0])
+    assert res.y == int(d["k_svd_y"])
+    _same_up_to_sign(res.columns.cpu().numpy(), d["k_svd_cols"], 1e-10)
+
+
+def test_deflation_compress_matches_reference(pk):
+    d = gio.load("next_strategies")
+    A = pk.linalg.as_matrix(gio.next_sequence(d)[0].A)
+    sink = pk.InstrumentationSink()
+    out = pk.deflation_compress(d["k_S"], A, 6, sink=sink)
+    np.testing.assert_allclose(out.spectrum, d["k_defl_mu"], rtol=1e-9)
+    _same_up_to_sign(out.Y_new.cpu().numpy(), d["k_defl_Y"], 1e-8)
+    assert out.stage1_width == 6 and out.enforced
+    assert sink.gram_assemblies == 1 and sink.matvecs == d["k_S"].shape[1]  # one assemble_gram
+
+
+def test_enforce_a_orthogonality(pk):
+    d = gio.load("next_strategies")
+    A = pk.linalg.as_matrix(gio.next_sequence(d)[0].A)
+    Y, L = pk.enforce_a_orthogonality(d["k_S"][:, :5], A)
+    G, _ = pk.assemble_gram(A, Y)
+    np.testing.assert_allclose(G.cpu().numpy(), np.eye(5), atol=1e-12)
+    # same range: Y L' reproduces the input
+    np.testing.assert_allclose(Y.cpu().numpy() @ L.full().T, d["k_S"][:, :5], rtol=1e-12, atol=1e-12)
+
+
+def test_ssor_apply_matches_reference(pk):
+    d = gio.load("next_strategies")
+    A = pk.linalg.as_matrix(gio.next_sequence(d)[0].A)
+    M = pk.build_preconditioner("ssor:1.3", A)
+    sink = pk.InstrumentationSink()
+    z = M.apply(d["k_ssor_r"], sink).cpu().numpy()
+    ref = d["k_ssor_z"]
+    np.testing.assert_allclose(z, ref, rtol=1e-12, atol=1e-14 * np.abs(ref).max())
+    assert sink.precond_applies == 1
+    with pytest.raises(pk.RecyklError):
+        pk.build_preconditioner("ssor:2.0", A)
+
+
+def test_ssor_on_elasticity_vs_oracle_and_deterministic(pk):
+    """Block-structured 3-D operator (Q1 elasticity, 1,944 rows): the sweeps
+    agree with the oracle's triangular solves and repeat bit for bit."""
+    from oracle import recycle_oracle as O
+    from paper_1512_05820_b200.problems import elasticity_sequence
+
+    H = next(iter(elasticity_sequence((8, 8, 8), p=1))).A
+    A = pk.SparseSpdMatrix(H.n, H.row_offsets, H.col_indices, H.values)
+    r = np.random.default_rng(2).standard_normal(H.n)
+    M = pk.build_preconditioner("ssor", A)
+    z1 = M.apply(r).cpu().numpy()
+    z2 = M.apply(torch.from_numpy(r).cuda()).cpu().numpy()
+    assert np.array_equal(z1, z2)
+    ref = O.Ssor(H.to_scipy(), 1.0)(r)
+    np.testing.assert_allclose(z1, ref, rtol=1e-11, atol=1e-13 * np.abs(ref).max())

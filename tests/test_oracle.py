@@ -161,3 +161,35 @@ def test_oracle_c5_small_pod():
     basis, sigma, y, _ = O.pod_from_gram(G, S, np.ones(256), 1.0)
     assert y == int(d["y"])
     np.testing.assert_allclose(sigma, d["sigma"], rtol=1e-10)
+
+
+@pytest.mark.parametrize("tag", list(gio.NEXT_CASES))
+def test_oracle_next_strategies(tag):
+    """output-metric POD, harmonic-Ritz deflation and SSOR
+    runs of the reference, replayed by the oracle (counters exact)."""
+    d = gio.load("next_strategies")
+    tr, mode, pc = gio.NEXT_CASES[tag]
+    xs, reps, _ = O.run_sequence(gio.next_sequence(d), O.Config(mode=mode, **tr), precond=pc)
+    _same(d, tag, xs, reps, xtol=1e-8 if pc.startswith("ssor") else 1e-10)
+
+
+def _same_up_to_sign(got, ref, tol):
+    for j in range(ref.shape[1]):
+        s = np.sign(got[:, j] @ ref[:, j])
+        assert np.linalg.norm(s * got[:, j] - ref[:, j]) <= tol * np.linalg.norm(ref[:, j]), j
+
+
+def test_oracle_next_kernels():
+    """pod_svd (pod.py:134-157), deflation_compress (truncation.py:152-188) and
+    one SSOR application (preconditioners.py:64-90) against the reference."""
+    d = gio.load("next_strategies")
+    A = O.as_csr(gio.next_sequence(d)[0].A)
+    basis, sigma, y, _ = O.pod_svd(d["k_S"], d["k_gamma"], d["C"], 1.0)
+    np.testing.assert_allclose(sigma, d["k_svd_sigma"], rtol=1e-12, atol=1e-14 * sigma[0])
+    assert y == int(d["k_svd_y"])
+    _same_up_to_sign(basis, d["k_svd_cols"], 1e-10)
+    Yo, _, mu = O.deflation(d["k_S"], A, 6, None, None)
+    np.testing.assert_allclose(mu, d["k_defl_mu"], rtol=1e-9)
+    _same_up_to_sign(Yo, d["k_defl_Y"], 1e-8)
+    z = O.Ssor(A, 1.3)(d["k_ssor_r"])
+    np.testing.assert_allclose(z, d["k_ssor_z"], rtol=1e-12, atol=1e-14 * np.abs(d["k_ssor_z"]).max())
