@@ -356,13 +356,64 @@ def run_next_strategies(rk):
     return {"next_strategies": d}
 
 
+BAD_MM = {
+    "bad_header.mtx": "%%MatrixMarket matrix coordinate complex symmetric\n2 2 1\n1 1 1.0\n",
+    "not_square.mtx": "%%MatrixMarket matrix coordinate real symmetric\n2 3 1\n1 1 1.0\n",
+    "too_many.mtx": "%%MatrixMarket matrix coordinate real symmetric\n2 2 1\n1 1 1.0\n2 2 1.0\n",
+    "too_few.mtx": "%%MatrixMarket matrix coordinate real symmetric\n2 2 3\n1 1 1.0\n2 2 1.0\n",
+    "out_of_range.mtx": "%%MatrixMarket matrix coordinate real symmetric\n2 2 2\n1 1 1.0\n3 2 1.0\n",
+    "malformed_entry.mtx": "%%MatrixMarket matrix coordinate real symmetric\n2 2 2\n1 1 1.0\n2 x 1.0\n",
+    "comments.mtx": "%%MatrixMarket matrix coordinate real symmetric\n% a comment\n\n2 2 3\n1 1 4.0\n"
+                    "% inner\n2 1 -1.0\n2 2 4.0\n",
+    "general_asym.mtx": "%%MatrixMarket matrix coordinate real general\n2 2 3\n1 1 4.0\n2 1 -1.0\n2 2 4.0\n",
+    "array_bad.mtx": "%%MatrixMarket matrix array real general\n3 1\n1.0\n2.0\n",
+    "array_ok.mtx": "%%MatrixMarket matrix array real general\n3 2\n1.0\n2.0\n3.0\n4.0\n5.0\n6.0\n",
+}
+
+
+def run_manifest(rk):
+    """a sequence written by the reference (write_sequence: JSON
+    manifest + Matrix Market files, kept under tests/golden/manifest_small/) with
+    the arrays the reference reads back, plus the reference's verdict (exception
+    type and message, paths relative) on malformed files (tests/golden/mm_cases/)."""
+    from recykl import mmio
+    from recykl.problems import gen_diffusion_sequence, gen_output_matrix, load_sequence_manifest, write_sequence
+
+    seq = gen_diffusion_sequence((6, 5), p=3, delta=0.1, seed=5, tol=1e-9)
+    seq.C = gen_output_matrix(2, seq.n, seed=7)
+    seq.systems[1].xbar = np.linspace(0.0, 1.0, seq.n)
+    mdir = os.path.join(OUT, "manifest_small")
+    write_sequence(seq, mdir, name="golden")
+    back = load_sequence_manifest(os.path.join(mdir, "manifest.json"))
+    d = _pack_sequence(back, "")
+    d["C"] = back.C
+    d["xbar2"] = back.systems[1].xbar
+    cdir = os.path.join(OUT, "mm_cases")
+    os.makedirs(cdir, exist_ok=True)
+    verdicts = {}
+    for name, text in BAD_MM.items():
+        path = os.path.join(cdir, name)
+        with open(path, "w") as fh:
+            fh.write(text)
+        reader = mmio.read_array if name.startswith("array") else mmio.read_matrix
+        try:
+            out = reader(path)
+            verdicts[name] = {"ok": True, "value": np.asarray(out.to_scipy().toarray() if hasattr(out, "to_scipy")
+                                                               else out).tolist()}
+        except Exception as exc:  # noqa: BLE001 - recording the reference's verdict
+            verdicts[name] = {"ok": False, "type": type(exc).__name__,
+                              "message": str(exc).replace(cdir + os.sep, "")}
+    d["verdicts_json"] = np.array(json.dumps(verdicts))
+    return {"manifest": d}
+
+
 def main():
     rk = _ref()
     os.makedirs(OUT, exist_ok=True)
     blobs = {}
     only = sys.argv[1:]
     runs = [run_fixture_cases, run_stage_variants, run_kernels, run_elasticity, run_c1, run_c2_small, run_c3_mid,
-            run_c5_small, run_next_strategies]
+            run_c5_small, run_next_strategies, run_manifest]
     for fn in runs:
         if not only or fn.__name__ in only:
             blobs.update(fn(rk))

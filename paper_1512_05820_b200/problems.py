@@ -436,3 +436,95 @@ def laplacian3d(nx: int, ny: int, nz: int) -> HostCsr:
 def snapshot_matrix(n: int, m: int, seed: int = 5) -> np.ndarray:
     """N(0,1) snapshot block S (n x m), host (for small parity sizes)."""
     return np.random.default_rng(seed).standard_normal((n, m))
+
+
+# ---------------------------------------------------------------------------
+# On-disk sequences: JSON manifest + Matrix Market files (problems.py:160-230)
+# ---------------------------------------------------------------------------
+def write_sequence(seq: SystemSequence, out_dir, name: str = "sequence") -> str:
+    """Matrix Market files plus a JSON manifest, the reference's layout and
+    file names (problems.py:160-187); returns the manifest path."""
+    import json
+    import os
+
+    from . import mmio
+
+    os.makedirs(out_dir, exist_ok=True)
+    entries = []
+    for j, spec in enumerate(seq, start=1):
+        mat_name, rhs_name = f"A_{j:03d}.mtx", f"b_{j:03d}.mtx"
+        mmio.write_symmetric_matrix(os.path.join(out_dir, mat_name), spec.A)
+        mmio.write_array(os.path.join(out_dir, rhs_name), np.asarray(spec.b))
+        entry = {"matrix": mat_name, "rhs": rhs_name, "tol": spec.tol}
+        if spec.xbar is not None:
+            guess_name = f"x_{j:03d}.mtx"
+            mmio.write_array(os.path.join(out_dir, guess_name), np.asarray(spec.xbar))
+            entry["guess"] = guess_name
+        entries.append(entry)
+    manifest = {"n": seq.n, "name": name, "systems": entries, "metadata": seq.metadata}
+    if seq.C is not None:
+        mmio.write_array(os.path.join(out_dir, "C.mtx"), seq.C)
+        manifest["output_matrix"] = "C.mtx"
+    path = os.path.join(out_dir, "manifest.json")
+    with open(path, "w") as fh:
+        json.dump(manifest, fh, indent=2)
+        fh.write("\n")
+    return path
+
+
+def load_sequence_manifest(path, *, lazy: bool = False) -> SystemSequence:
+    """A sequence described by a JSON manifest (problems.py:190-230), same
+    checks and ManifestError messages. ``lazy`` defers reading each system's
+    files to iteration time, so ``run_sequence`` parses and uploads system j+1
+    on its helper thread while system j solves (nothing but the current and
+    the next system is held in host memory)."""
+    import json
+    import os
+
+    from . import mmio
+    from .errors import ManifestError
+
+    try:
+        with open(path) as fh:
+            manifest = json.load(fh)
+    except json.JSONDecodeError as exc:
+        raise ManifestError(f"{path}:{exc.lineno}: invalid JSON ({exc.msg})") from exc
+    base = os.path.dirname(os.path.abspath(path))
+    try:
+        n = int(manifest["n"])
+        raw_systems = manifest["systems"]
+    except (KeyError, TypeError, ValueError) as exc:
+        raise ManifestError(f"{path}: manifest must carry 'n' and 'systems'") from exc
+    parsed = []
+    for idx, entry in enumerate(raw_systems, start=1):
+        try:
+            parsed.append((entry["matrix"], entry["rhs"], float(entry.get("tol", 1e-8)), entry.get("guess")))
+        except (KeyError, TypeError, ValueError) as exc:
+            raise ManifestError(f"{path}: system {idx} entry malformed") from exc
+
+    def load(idx, mat_file, rhs_file, tol, guess):
+        A = mmio.read_matrix(os.path.join(base, mat_file))
+        b = mmio.read_array(os.path.join(base, rhs_file))
+        if A.n != n or b.shape[0] != n:
+            raise ManifestError(
+                f"{path}: system {idx} dimension mismatch (matrix {A.n}, rhs {b.shape[0]}, manifest {n})")
+        xbar = None
+        if guess is not None:
+            xbar = mmio.read_array(os.path.join(base, guess))
+            if xbar.shape[0] != n:
+                raise ManifestError(f"{path}: system {idx} guess has wrong length")
+        return LinearSystemSpec(A=A, b=np.asarray(b), xbar=xbar, tol=tol)
+
+    if lazy:
+        def systems():
+            for idx, item in enumerate(parsed, start=1):
+                yield load(idx, *item)
+    else:
+        systems = [load(idx, *item) for idx, item in enumerate(parsed, start=1)]
+    C = None
+    if manifest.get("output_matrix"):
+        C = np.atleast_2d(mmio.read_array(os.path.join(base, manifest["output_matrix"])))
+        if C.shape[1] != n:
+            raise ManifestError(f"{path}: output matrix has {C.shape[1]} columns, expected {n}")
+    meta = manifest.get("metadata", {"name": manifest.get("name")})
+    return SystemSequence(n=n, systems=systems, C=C, metadata=meta, p_hint=len(parsed))

@@ -100,3 +100,23 @@ def test_ssor_on_elasticity_vs_oracle_and_deterministic(pk):
     assert np.array_equal(z1, z2)
     ref = O.Ssor(H.to_scipy(), 1.0)(r)
     np.testing.assert_allclose(z1, ref, rtol=1e-11, atol=1e-13 * np.abs(ref).max())
+
+
+def test_manifest_sequence_on_device(pk):
+    """f1: a reference-written manifest, loaded lazily (parse + upload of system
+    j+1 on the helper thread while j solves), gives bit-identical solutions to
+    the same arrays handed over in memory."""
+    import os
+
+    from paper_1512_05820_b200.problems import load_sequence_manifest
+
+    d = gio.load("manifest")
+    tr = dict(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=8, max_dim=6)
+    lazy = load_sequence_manifest(os.path.join(gio.GOLDEN, "manifest_small", "manifest.json"), lazy=True)
+    xs1, reps1, _ = _run(pk, lazy, tr, "cg", "jacobi")
+    mem = gio.sequence(d)
+    mem.systems[1].xbar = d["xbar2"]
+    xs2, reps2, _ = _run(pk, mem, tr, "cg", "jacobi")
+    assert [r.stage3_iters for r in reps1] == [r.stage3_iters for r in reps2]
+    for a, b in zip(xs1, xs2):
+        assert torch.equal(a, b)
