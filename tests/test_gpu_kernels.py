@@ -124,6 +124,22 @@ def test_sell_spmv_fma_chain_at_c3_size(pk):
     assert np.array_equal(res.AV[:, 0].cpu().numpy()[rows], _fma_chain_rows(H, p0, rows))
 
 
+def test_sell_spmm_columns_are_bitwise_spmv(pk):
+    """K2 on the 3x3 SELL view: every column of A X is bitwise the SpMV of that
+    column (same fma chain), for widths that exercise full and ragged tiles."""
+    from paper_1512_05820_b200.linalg import as_block, spmm
+    from paper_1512_05820_b200.problems import elasticity_sequence
+
+    H = next(iter(elasticity_sequence((7, 5, 6), p=1))).A
+    A = pk.SparseSpdMatrix(H.n, H.row_offsets, H.col_indices, H.values)
+    assert A.bval is not None
+    for m in (1, 5, 8, 13):
+        X = np.random.default_rng(m).standard_normal((H.n, m))
+        Y = spmm(A, as_block(X)).cpu().numpy()
+        for j in range(m):
+            assert np.array_equal(Y[:, j], pk.spmv(A, X[:, j]).cpu().numpy()), (m, j)
+
+
 def test_spmv_sink_counts_one_matvec(pk):
     A = pk.SparseSpdMatrix.identity(5)
     sink = pk.InstrumentationSink()
