@@ -127,7 +127,8 @@ typedef struct rk_pcg_plan {
   int64_t partials_len;
   uint32_t* tickets;        /* RK_PCG_TICKETS zero-initialised counters */
   int32_t mode;             /* 0 cg, 1 fom (two CGS sweeps), 2 fom with paper beta */
-  int32_t pad_;
+  int32_t linv_full;        /* 1: L holds F^{-1} = L^{-T} L^{-1} of the dense block (full,
+                             * symmetric); 0: L holds L^{-1} (lower triangular) */
 } rk_pcg_plan;
 
 const char* rk_last_error(void);

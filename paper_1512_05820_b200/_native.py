@@ -94,7 +94,7 @@ class RkPcgPlan(ctypes.Structure):
         ("partials_len", c_i64),
         ("tickets", c_vp),
         ("mode", c_i32),
-        ("pad_", c_i32),
+        ("linv_full", c_i32),
     ]
 
 

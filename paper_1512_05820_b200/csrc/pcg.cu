@@ -62,11 +62,11 @@ constexpr int kFuseMax = 64;                     // widths whose finish runs in 
 constexpr int kMaxGroups = 256;                  // chunk groups of the fused two-level combine
 
 // mu = F^{-1} c with F = blockdiag(L L', diag(sqd)^2) (krylov.py:119-132
-// BlockDiagFactor.solve_spd). P.L holds Linv = L^{-1} (lower triangular, from
-// LAPACK dtrtri on the host), so the two triangular solves become two
-// triangular mat-vecs, y = Linv c and mu = Linv' y, one output per thread
-// (instead of a chain of w dependent substitution steps); the diagonal block
-// is a division.
+// BlockDiagFactor.solve_spd). P.L holds either Linv = L^{-1} (linv_full = 0;
+// lower triangular, LAPACK dtrtri on the host: the two triangular solves become
+// two triangular mat-vecs, y = Linv c and mu = Linv' y) or the dense block's
+// F^{-1} = Linv' Linv (linv_full = 1, one symmetric mat-vec: half the
+// dependent steps in the latency-bound tail); the diagonal block is a division.
 __device__ void solve_factor(const rk_pcg_plan& P, const double* c, double* ysm, const double* Ls, double* mu) {
   const int64_t w = P.wchol, m = P.m;
   // Linv is either staged in shared memory (Ls, ld = w, zero above the
@@ -74,6 +74,22 @@ __device__ void solve_factor(const rk_pcg_plan& P, const double* c, double* ysm,
   // place: each thread's row loads are independent, so they are all in flight.
   const double* __restrict__ L = Ls ? Ls : P.L;
   const int64_t ldl = Ls ? w : P.ldl;
+  if (P.linv_full) {  // L holds F^{-1}: one symmetric mat-vec (row i = column i)
+    for (int64_t i = threadIdx.x; i < w; i += blockDim.x) {
+      double s = 0.0;
+      for (int64_t j = 0; j < w; ++j) s = fma(L[j + i * ldl], c[j], s);
+      ysm[i + w] = s;
+    }
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+      if (i < w) mu[i] = ysm[i + w];
+      else {
+        const double d = P.sqd[i - w];
+        mu[i] = c[i] / (d * d);
+      }
+    }
+    return;
+  }
   for (int64_t i = threadIdx.x; i < w; i += blockDim.x) {   // y = Linv c
     double s = 0.0;
     for (int64_t j = 0; j <= i; ++j) s = fma(L[i + j * ldl], c[j], s);
@@ -108,6 +124,32 @@ __device__ void solve_factor_warps(const rk_pcg_plan& P, const double* c, double
   double a[R], lv[R];
 #pragma unroll
   for (int q = 0; q < R; ++q) a[q] = 0.0;
+  if (P.linv_full) {  // mu_i = sum_j Finv[j, i] c_j (column i: coalesced), one pass
+    for (int t = 0; 32 * t < w; ++t) {
+      const int j = lane + 32 * t;
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int i = warp + 8 * q;
+        lv[q] = (i < w && j < w) ? __ldg(L + j + (int64_t)i * ldl) : 0.0;
+      }
+      const double cj = j < w ? c[j] : 0.0;
+#pragma unroll
+      for (int q = 0; q < R; ++q) a[q] = fma(lv[q], cj, a[q]);
+    }
+    warp_sum_n(a);
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int i = warp + 8 * q;
+      if (lane == 0 && i < w) mu[i] = a[q];
+    }
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+      if (i >= w) {
+        const double d = P.sqd[i - w];
+        mu[i] = c[i] / (d * d);
+      }
+    }
+    return;
+  }
   for (int t = 0; 32 * t < w; ++t) {  // y_i = sum_{j <= i} Linv[i, j] c_j
     const int j = lane + 32 * t;
 #pragma unroll
@@ -388,7 +430,7 @@ __global__ void __launch_bounds__(256) k_pcg_finish(const rk_pcg_plan P, int ent
   if (staged) {
     for (int64_t e = threadIdx.x; e < w * w; e += blockDim.x) {
       const int64_t col = e / w, row = e - col * w;
-      Ls[e] = row >= col ? P.L[row + col * P.ldl] : 0.0;
+      Ls[e] = (P.linv_full || row >= col) ? P.L[row + col * P.ldl] : 0.0;
     }
   }
   pdl_wait();

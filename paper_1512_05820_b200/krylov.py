@@ -176,8 +176,9 @@ class BlockDiagFactor:
         return out
 
     def device_form(self, device):
-        """(L, wchol, sqd) for the fused kernels: one leading dense block and a
-        trailing sqrt-diagonal; other block patterns are densified."""
+        """(F^{-1} of the dense block, wchol, sqd, full=True) for the fused
+        kernels: one leading dense block and a trailing sqrt-diagonal; other
+        block patterns are densified."""
         key = (device.type, device.index)
         hit = self._dev.get(key)
         if hit is not None:
@@ -187,14 +188,14 @@ class BlockDiagFactor:
             if kinds and kinds[0] == "chol":
                 L = self._blocks[0][1]
                 w = L.m
-                Ld = L.device_inverse(device)
+                Ld = L.device_spd_inverse(device)
                 rest = [b for _, b in self._blocks[1:]]
             else:
                 w, Ld = 0, None
                 rest = [b for _, b in self._blocks]
             sqd = np.concatenate(rest) if rest else np.zeros(0)
             sqd_d = torch.from_numpy(np.ascontiguousarray(sqd)).to(device) if sqd.size else None
-            out = (Ld, w, sqd_d)
+            out = (Ld, w, sqd_d, True)
         else:
             Lfull = np.zeros((self.size, self.size))
             at = 0
@@ -206,8 +207,8 @@ class BlockDiagFactor:
                     m = block.shape[0]
                     Lfull[np.arange(at, at + m), np.arange(at, at + m)] = block
                     at += m
-            Linv = DenseLowerTriangular.from_full(Lfull).device_inverse(device)
-            out = (Linv, self.size, None)
+            Finv = DenseLowerTriangular.from_full(Lfull).device_spd_inverse(device)
+            out = (Finv, self.size, None, True)
         self._dev[key] = out
         return out
 
@@ -327,9 +328,11 @@ class _Run:
         P = self.plan
         if B is None:
             P.m, P.B, P.ldb, P.cross, P.ldc, P.L, P.ldl, P.wchol, P.sqd = 0, None, 0, None, 0, None, 0, 0, None
+            P.linv_full = 0
             return
         self._keep = (B, cross, factor_dev)
-        L, w, sqd = factor_dev
+        L, w, sqd = factor_dev[:3]
+        P.linv_full = 1 if len(factor_dev) > 3 and factor_dev[3] else 0
         P.m = int(B.shape[1])
         P.B, P.ldb = B.data_ptr(), block_ld(B)
         P.cross, P.ldc = cross.data_ptr(), block_ld(cross)

@@ -764,9 +764,22 @@ class DenseLowerTriangular:
             t = self._dev[key] = as_block(np.tril(Linv), device)
         return t
 
+    def device_spd_inverse(self, device) -> torch.Tensor:
+        """Column-major device copy of F^{-1} = L^{-T} L^{-1} (host dtrtri, then a
+        w x w product): the fused kernels apply it as one symmetric mat-vec."""
+        key = ("spdinv", device.type, device.index)
+        t = self._dev.get(key)
+        if t is None:
+            Linv, info = scipy.linalg.lapack.dtrtri(self._full, lower=1)
+            if info != 0:
+                raise NotPositiveDefinite("singular Cholesky factor", pivot=int(info - 1) if info > 0 else None)
+            Linv = np.tril(Linv)
+            t = self._dev[key] = as_block(Linv.T @ Linv, device)
+        return t
+
     def device_form(self, device):
-        """(Linv, w, sqd=None) in the form the fused PCG kernels take."""
-        return (self.device_inverse(device) if self.m else None, self.m, None)
+        """(F^{-1}, w, sqd=None, full=True) in the form the fused PCG kernels take."""
+        return (self.device_spd_inverse(device) if self.m else None, self.m, None, True)
 
     def solve_lower(self, rhs):
         return scipy.linalg.solve_triangular(self._full, np.asarray(rhs, dtype=np.float64), lower=True)
