@@ -440,7 +440,9 @@ def augmented_pcg(
     m = int(Y.shape[1]) if Y is not None else 0
     keep_av = code == 1 or keep_products
     max_iter = n if max_iter is None else int(max_iter)
-    run = _Run(n, device, max(code, 0), keep_av, m if direct else 0, vcap=min(max_iter + 2, 64))
+    hint_key = (n, device.index, keep_av)
+    vcap = min(max_iter + 2, max(64, _CAP_HINT.get(hint_key, 0)))
+    run = _Run(n, device, max(code, 0), keep_av, m if direct else 0, vcap=vcap)
 
     if Y is not None:
         gemv_n(Y, yh, out=run.x)
@@ -608,7 +610,15 @@ def _count_matvecs(operator, count):
         operator.sink.add_matvec(count)
 
 
+# Direction-block capacity from the previous runs of the same size: a sequence's
+# systems take similar iteration counts, so V / AV are allocated once at the
+# right width instead of growing by doubling (a copy of both blocks per step).
+_CAP_HINT: dict = {}
+
+
 def _result(run: _Run, k: int, converged: bool) -> AugmentedPcgResult:
+    key = (run.n, run.device.index, run.keep_av)
+    _CAP_HINT[key] = max(_CAP_HINT.get(key, 0), min(int(1.25 * k) + 8, 1 << 16))
     alphas, gammas, hist = run.histories(k)
     res = AugmentedPcgResult(
         k=k, vhat=alphas, V=run.V[:, :k], gamma=gammas, residual_history=hist, x=run.x, converged=converged
