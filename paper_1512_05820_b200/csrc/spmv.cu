@@ -285,6 +285,57 @@ __global__ void __launch_bounds__(256) k_csr_asymmetry(int64_t n, const int32_t*
 // lane. 76 bytes per stored block (vs 108 for the same 9
 // nonzeros in CSR); slices are padded only to their widest row.
 // ---------------------------------------------------------------------------
+// Software-pipelined variant (U = 0), two stages: while the fmas of slot row t
+// run, the x gather of slot row t+1 (whose block column arrived an iteration
+// ago) and the column + values of slot row t+2 are in flight, so in-order
+// issue never waits on a load issued in the same iteration.
+__device__ __forceinline__ void sell3_row_pipe(const rk_csr& A, const double* __restrict__ x, int64_t slice,
+                                               int lane, double& s0, double& s1, double& s2) {
+  s0 = s1 = s2 = 0.0;
+  const int32_t base = __ldg(A.browptr + slice);
+  const int32_t width = (__ldg(A.browptr + slice + 1) - base) >> 5;
+  if (width == 0) return;
+  const int32_t* __restrict__ col = A.bcol + base + lane;
+  const double* __restrict__ val = A.bval + 9 * (int64_t)base + lane;
+  double v0[9], v1[9], v2[9], x0[3], x1[3];
+  int32_t c1 = 0, c2 = 0;
+  // prologue: slot 0 gathered, slot 1 loaded
+  {
+    const int32_t c0 = __ldcs(col);
+#pragma unroll
+    for (int e = 0; e < 9; ++e) v0[e] = __ldcs(val + 32 * e);
+    if (width > 1) {
+      c1 = __ldcs(col + 32);
+#pragma unroll
+      for (int e = 0; e < 9; ++e) v1[e] = __ldcs(val + 288 + 32 * e);
+    }
+    const double* xp = x + 3 * (int64_t)c0;
+    x0[0] = __ldg(xp); x0[1] = __ldg(xp + 1); x0[2] = __ldg(xp + 2);
+  }
+  for (int32_t t = 0; t < width; ++t) {
+    if (t + 1 < width) {  // gather for slot t+1
+      const double* xp = x + 3 * (int64_t)c1;
+      x1[0] = __ldg(xp); x1[1] = __ldg(xp + 1); x1[2] = __ldg(xp + 2);
+    }
+    if (t + 2 < width) {  // column + values for slot t+2
+      c2 = __ldcs(col + 32 * (t + 2));
+#pragma unroll
+      for (int e = 0; e < 9; ++e) v2[e] = __ldcs(val + 288 * (t + 2) + 32 * e);
+    }
+    s0 = fma(v0[0], x0[0], s0); s0 = fma(v0[1], x0[1], s0); s0 = fma(v0[2], x0[2], s0);
+    s1 = fma(v0[3], x0[0], s1); s1 = fma(v0[4], x0[1], s1); s1 = fma(v0[5], x0[2], s1);
+    s2 = fma(v0[6], x0[0], s2); s2 = fma(v0[7], x0[1], s2); s2 = fma(v0[8], x0[2], s2);
+#pragma unroll
+    for (int e = 0; e < 9; ++e) {
+      v0[e] = v1[e];
+      v1[e] = v2[e];
+    }
+    x0[0] = x1[0]; x0[1] = x1[1]; x0[2] = x1[2];
+    c1 = c2;
+  }
+}
+
+template <int U>
 __device__ __forceinline__ void sell3_row(const rk_csr& A, const double* __restrict__ x, int64_t slice, int lane,
                                           double& s0, double& s1, double& s2) {
   s0 = s1 = s2 = 0.0;
@@ -294,26 +345,31 @@ __device__ __forceinline__ void sell3_row(const rk_csr& A, const double* __restr
   // slot row t of the slice: 9 x 32 values, contiguous (entry e at 32 e + lane)
   const double* __restrict__ val = A.bval + 9 * (int64_t)base + lane;
   int32_t t = 0;
-  for (; t + 2 <= width; t += 2) {  // two slots in flight per lane
-    const int32_t ca = __ldcs(col + 32 * t), cb = __ldcs(col + 32 * (t + 1));
-    double va[9], vb[9];
+  for (; t + U <= width; t += U) {  // U slot rows in flight per lane
+    int32_t c[U];
+    double v[U][9];
 #pragma unroll
-    for (int e = 0; e < 9; ++e) {
-      va[e] = __ldcs(val + 288 * t + 32 * e);
-      vb[e] = __ldcs(val + 288 * (t + 1) + 32 * e);
+    for (int u = 0; u < U; ++u) c[u] = __ldcs(col + 32 * (t + u));
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int e = 0; e < 9; ++e) v[u][e] = __ldcs(val + 288 * (t + u) + 32 * e);
+    double xs[U][3];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double* xc = x + 3 * (int64_t)c[u];
+      xs[u][0] = __ldg(xc);
+      xs[u][1] = __ldg(xc + 1);
+      xs[u][2] = __ldg(xc + 2);
     }
-    const double* xa = x + 3 * (int64_t)ca;
-    const double* xb = x + 3 * (int64_t)cb;
-    const double a0 = __ldg(xa), a1 = __ldg(xa + 1), a2 = __ldg(xa + 2);
-    const double b0 = __ldg(xb), b1 = __ldg(xb + 1), b2 = __ldg(xb + 2);
-    s0 = fma(va[0], a0, s0); s0 = fma(va[1], a1, s0); s0 = fma(va[2], a2, s0);
-    s1 = fma(va[3], a0, s1); s1 = fma(va[4], a1, s1); s1 = fma(va[5], a2, s1);
-    s2 = fma(va[6], a0, s2); s2 = fma(va[7], a1, s2); s2 = fma(va[8], a2, s2);
-    s0 = fma(vb[0], b0, s0); s0 = fma(vb[1], b1, s0); s0 = fma(vb[2], b2, s0);
-    s1 = fma(vb[3], b0, s1); s1 = fma(vb[4], b1, s1); s1 = fma(vb[5], b2, s1);
-    s2 = fma(vb[6], b0, s2); s2 = fma(vb[7], b1, s2); s2 = fma(vb[8], b2, s2);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {  // slots in order: the same fma chain for every U
+      s0 = fma(v[u][0], xs[u][0], s0); s0 = fma(v[u][1], xs[u][1], s0); s0 = fma(v[u][2], xs[u][2], s0);
+      s1 = fma(v[u][3], xs[u][0], s1); s1 = fma(v[u][4], xs[u][1], s1); s1 = fma(v[u][5], xs[u][2], s1);
+      s2 = fma(v[u][6], xs[u][0], s2); s2 = fma(v[u][7], xs[u][1], s2); s2 = fma(v[u][8], xs[u][2], s2);
+    }
   }
-  if (t < width) {
+  for (; t < width; ++t) {
     const int32_t ca = __ldcs(col + 32 * t);
     double va[9];
 #pragma unroll
@@ -334,7 +390,7 @@ __global__ void __launch_bounds__(kSpmvThreads) k_bsr3_spmv(const rk_csr A, cons
   const int64_t wpb = kSpmvThreads / 32;
   for (int64_t sl = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); sl < nsl; sl += (int64_t)gridDim.x * wpb) {
     double s0, s1, s2;
-    sell3_row(A, x, sl, lane, s0, s1, s2);
+    sell3_row<2>(A, x, sl, lane, s0, s1, s2);
     const int64_t br = sl * 32 + lane;
     if (br < nbr) {
       y[3 * br] = s0;
@@ -344,6 +400,7 @@ __global__ void __launch_bounds__(kSpmvThreads) k_bsr3_spmv(const rk_csr A, cons
   }
 }
 
+template <int U>
 __global__ void __launch_bounds__(kSpmvThreads) k_bsr3_spmv_pcg(const rk_pcg_plan P) {
   pdl_wait();
   pdl_trigger();
@@ -359,7 +416,8 @@ __global__ void __launch_bounds__(kSpmvThreads) k_bsr3_spmv_pcg(const rk_pcg_pla
   double acc[2] = {0.0, 0.0};
   for (int64_t sl = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); sl < nsl; sl += (int64_t)gridDim.x * wpb) {
     double s0, s1, s2;
-    sell3_row(P.A, p, sl, lane, s0, s1, s2);
+    if constexpr (U == 0) sell3_row_pipe(P.A, p, sl, lane, s0, s1, s2);
+    else sell3_row<U>(P.A, p, sl, lane, s0, s1, s2);
     const int64_t br = sl * 32 + lane;
     if (br < nbr) {
       const int64_t row = 3 * br;
@@ -478,14 +536,36 @@ static int launch_bsr3_spmv(const rk_csr& A, const double* x, double* y, cudaStr
   return cuda_check("rk_spmv (bsr3)");
 }
 
-static void launch_bsr3_spmv_pcg(const rk_pcg_plan& P, cudaStream_t s) {
+template <int U>
+static void launch_bsr3_spmv_pcg_u(const rk_pcg_plan& P, cudaStream_t s) {
   // a fixed number of blocks per SM (when resident), so the order of the
   // p'Ap / p'p partial sums does not follow register allocation
-  static const int cap = std::min(resident_blocks((const void*)rk::k_bsr3_spmv_pcg, rk::kSpmvThreads),
+  static const int cap = std::min(resident_blocks((const void*)rk::k_bsr3_spmv_pcg<U>, rk::kSpmvThreads),
                                   sm_count() * spmv_blocks_per_sm());
   const int64_t need = ((P.n / 3 + 31) / 32 + rk::kSpmvThreads / 32 - 1) / (rk::kSpmvThreads / 32);
-  launch_pdl(rk::k_bsr3_spmv_pcg, dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(cap, need))),
+  launch_pdl(rk::k_bsr3_spmv_pcg<U>, dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(cap, need))),
              dim3(rk::kSpmvThreads), 0, s, P);
+}
+
+static int sell_unroll() {
+  static const int v = [] {
+    const char* e = getenv("RK_SELL_U");
+    // 2 slot rows in flight (default); 0 = two-stage software pipeline (3% faster
+    // in isolation, equal inside the sequence, and 128 registers)
+    const int x = e ? atoi(e) : 2;
+    return (x >= 0 && x <= 4) ? x : 2;
+  }();
+  return v;
+}
+
+static void launch_bsr3_spmv_pcg(const rk_pcg_plan& P, cudaStream_t s) {
+  switch (sell_unroll()) {
+    case 0: launch_bsr3_spmv_pcg_u<0>(P, s); break;
+    case 1: launch_bsr3_spmv_pcg_u<1>(P, s); break;
+    case 3: launch_bsr3_spmv_pcg_u<3>(P, s); break;
+    case 4: launch_bsr3_spmv_pcg_u<4>(P, s); break;
+    default: launch_bsr3_spmv_pcg_u<2>(P, s); break;
+  }
 }
 
 int launch_bsr3_gather(int64_t nblk, const int32_t* perm, const double* val, double* bval, cudaStream_t s) {
