@@ -28,5 +28,11 @@ class phase:
         return False
 
 
+def add(name: str, seconds: float) -> None:
+    """Accumulate a host-side wall interval (no device synchronisation)."""
+    if ENABLED:
+        TIMES[name] = TIMES.get(name, 0.0) + seconds
+
+
 def reset():
     TIMES.clear()
