@@ -61,25 +61,30 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* scratch) {
 
 // Publish this block's partials and find out whether it is the last block to
 // finish. partials is [gridDim.x][nv]; the ticket is reset by the last block.
+// Release/acquire at GPU scope by thread 0 around the ticket (the barrier
+// orders the block's writes before the release).
 __device__ __forceinline__ bool publish_and_check_last(const double* vals, int nv,
                                                        double* partials, uint32_t* ticket) {
   __shared__ bool s_last;
   for (int j = threadIdx.x; j < nv; j += blockDim.x)
     partials[(int64_t)blockIdx.x * nv + j] = vals[j];
-  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
+    asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
     uint32_t t = atomicAdd(ticket, 1u);
     s_last = (t == gridDim.x - 1);
-    if (s_last) *ticket = 0u;
+    if (s_last) {
+      *ticket = 0u;
+      asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+    }
   }
   __syncthreads();
-  if (s_last) __threadfence();
   return s_last;
 }
 
 // Last block: out[j] = sum over blocks (fixed order) of partials[b][j], j < nv.
 // One warp per value, lanes stride over blocks, then a butterfly: deterministic.
+// (A block-parallel variant measured slower inside the SpMV: kept simple.)
 __device__ __forceinline__ void combine_partials(const double* partials, int nb, int nv,
                                                  double* out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
