@@ -131,19 +131,43 @@ def as_block(B, device=None) -> torch.Tensor:
 
 
 _STAGE_MIN_BYTES = 1 << 22
+_STAGE_CHUNK = 32 << 20  # bytes per staging chunk of large uploads
+_stage_pool = None
+_stage_pool_lock = threading.Lock()
+
+
+def _staging_pool():
+    global _stage_pool
+    with _stage_pool_lock:
+        if _stage_pool is None:
+            import concurrent.futures
+
+            _stage_pool = concurrent.futures.ThreadPoolExecutor(max_workers=4, thread_name_prefix="rk-stage")
+        return _stage_pool
 
 
 def host_to_device(arr: np.ndarray, device, dtype=np.float64) -> torch.Tensor:
     """H2D copy of a host array. Large arrays are staged through pinned memory
-    with np.copyto (which releases the GIL) and sent with an asynchronous DMA, so
-    a prefetching helper thread does not stall the thread launching kernels; the
-    torch host allocator keeps the pinned block alive until the copy is done."""
+    in 32 MB chunks copied by a small thread pool (np.copyto releases the GIL)
+    and each chunk's asynchronous DMA is queued as soon as it is staged, so the
+    host copy, the DMA and the device work of the launching thread overlap; the
+    torch host allocator keeps the pinned block alive until the copies are done."""
     a = np.ascontiguousarray(np.asarray(arr, dtype=dtype))
     if a.nbytes < _STAGE_MIN_BYTES:
         return torch.from_numpy(a).to(device)
-    stage = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, pin_memory=True)
-    np.copyto(stage.numpy(), a)
-    return stage.to(device, non_blocking=True)
+    tdtype = torch.from_numpy(a[:0]).dtype
+    stage = torch.empty(a.shape, dtype=tdtype, pin_memory=True)
+    out = torch.empty(a.shape, dtype=tdtype, device=device)
+    flat_a, flat_s, flat_o = a.reshape(-1), stage.reshape(-1), out.reshape(-1)
+    step = max(1, _STAGE_CHUNK // a.itemsize)
+    bounds = [(i, min(i + step, flat_a.size)) for i in range(0, flat_a.size, step)]
+    sv = flat_s.numpy()
+    pool = _staging_pool()
+    futures = [pool.submit(np.copyto, sv[lo:hi], flat_a[lo:hi]) for lo, hi in bounds]
+    for (lo, hi), fut in zip(bounds, futures):
+        fut.result()
+        flat_o[lo:hi].copy_(flat_s[lo:hi], non_blocking=True)
+    return out
 
 
 def as_vector(x, device=None, copy: bool = False) -> torch.Tensor:
