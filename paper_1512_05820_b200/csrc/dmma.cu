@@ -18,7 +18,13 @@ namespace rk {
 
 constexpr int kTile = 64;
 constexpr int kStep = 16;             // K rows per pipeline stage
-constexpr int kStages = 4;
+#ifndef RK_GRAM_STAGES
+#define RK_GRAM_STAGES 4
+#endif
+#ifndef RK_GRAM_MINB
+#define RK_GRAM_MINB 2
+#endif
+constexpr int kStages = RK_GRAM_STAGES;
 constexpr int kPadK = kStep + 4;      // 20 doubles: conflict-free 8-byte fragment loads
 constexpr int kPadM = kTile + 4;      // 68 doubles: conflict-free for the S tile of K8
 constexpr int kDmmaThreads = 128;
@@ -40,7 +46,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // --------------------------------------------------------------------------
 // K7: out[split] (m1 x m2 tile region, col-major ldo) = X[kbeg:kend, :]' Y[kbeg:kend, :]
 // --------------------------------------------------------------------------
-__global__ void __launch_bounds__(kDmmaThreads, 2)
+__global__ void __launch_bounds__(kDmmaThreads, RK_GRAM_MINB)
     k_gram(int64_t n, int64_t m1, const double* __restrict__ X, int64_t ldx, int64_t m2,
            const double* __restrict__ Y, int64_t ldy, double* __restrict__ out, int64_t ldo,
            int64_t split_stride, int64_t rows_per_split, int64_t upper_off) {
@@ -260,7 +266,15 @@ static GramGeom gram_geometry(int64_t n, int64_t m1, int64_t m2, int64_t upper_o
   g.ta = (m1 + rk::kTile - 1) / rk::kTile;
   g.tb = (m2 + rk::kTile - 1) / rk::kTile;
   const int64_t tiles = std::max<int64_t>(1, active_tiles(g.ta, g.tb, upper_off));
-  const int64_t slots = (int64_t)sm_count() * 2;
+  static const int64_t per_sm = [] {
+    int occ = 0;
+    cudaFuncSetAttribute(rk::k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem());
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rk::k_gram, rk::kDmmaThreads, gram_smem()) != cudaSuccess ||
+        occ < 1)
+      occ = 2;
+    return (int64_t)occ;
+  }();
+  const int64_t slots = (int64_t)sm_count() * per_sm;
   const int64_t max_splits = std::max<int64_t>(1, n / 512);
   double fill[9] = {0};
   int64_t pick[9] = {0};

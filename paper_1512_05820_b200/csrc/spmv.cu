@@ -335,6 +335,66 @@ __device__ __forceinline__ void sell3_row_pipe(const rk_csr& A, const double* __
   }
 }
 
+// Streaming loads the compiler may not reorder among themselves (volatile asm):
+// with them, every column and value load of U slot rows is issued before the
+// first dependent gather, whatever the scheduler's register heuristics.
+__device__ __forceinline__ double ld_stream_f64(const double* p) {
+  double v;
+  asm volatile("ld.global.cs.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int32_t ld_stream_s32(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.global.cs.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+template <int U>
+__device__ __forceinline__ void sell3_row_issue(const rk_csr& A, const double* __restrict__ x, int64_t slice,
+                                                int lane, double& s0, double& s1, double& s2) {
+  s0 = s1 = s2 = 0.0;
+  const int32_t base = __ldg(A.browptr + slice);
+  const int32_t width = (__ldg(A.browptr + slice + 1) - base) >> 5;
+  const int32_t* __restrict__ col = A.bcol + base + lane;
+  const double* __restrict__ val = A.bval + 9 * (int64_t)base + lane;
+  int32_t t = 0;
+  for (; t + U <= width; t += U) {
+    int32_t c[U];
+    double v[U][9];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = ld_stream_s32(col + 32 * (t + u));
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int e = 0; e < 9; ++e) v[u][e] = ld_stream_f64(val + 288 * (t + u) + 32 * e);
+    double xs[U][3];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double* xc = x + 3 * (int64_t)c[u];
+      xs[u][0] = __ldg(xc);
+      xs[u][1] = __ldg(xc + 1);
+      xs[u][2] = __ldg(xc + 2);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      s0 = fma(v[u][0], xs[u][0], s0); s0 = fma(v[u][1], xs[u][1], s0); s0 = fma(v[u][2], xs[u][2], s0);
+      s1 = fma(v[u][3], xs[u][0], s1); s1 = fma(v[u][4], xs[u][1], s1); s1 = fma(v[u][5], xs[u][2], s1);
+      s2 = fma(v[u][6], xs[u][0], s2); s2 = fma(v[u][7], xs[u][1], s2); s2 = fma(v[u][8], xs[u][2], s2);
+    }
+  }
+  for (; t < width; ++t) {
+    const int32_t ca = ld_stream_s32(col + 32 * t);
+    double va[9];
+#pragma unroll
+    for (int e = 0; e < 9; ++e) va[e] = ld_stream_f64(val + 288 * t + 32 * e);
+    const double* xa = x + 3 * (int64_t)ca;
+    const double a0 = __ldg(xa), a1 = __ldg(xa + 1), a2 = __ldg(xa + 2);
+    s0 = fma(va[0], a0, s0); s0 = fma(va[1], a1, s0); s0 = fma(va[2], a2, s0);
+    s1 = fma(va[3], a0, s1); s1 = fma(va[4], a1, s1); s1 = fma(va[5], a2, s1);
+    s2 = fma(va[6], a0, s2); s2 = fma(va[7], a1, s2); s2 = fma(va[8], a2, s2);
+  }
+}
+
 template <int U>
 __device__ __forceinline__ void sell3_row(const rk_csr& A, const double* __restrict__ x, int64_t slice, int lane,
                                           double& s0, double& s1, double& s2) {
@@ -382,7 +442,7 @@ __device__ __forceinline__ void sell3_row(const rk_csr& A, const double* __restr
   }
 }
 
-__global__ void __launch_bounds__(kSpmvThreads) k_bsr3_spmv(const rk_csr A, const double* __restrict__ x,
+__global__ void __launch_bounds__(kSpmvThreads, 2) k_bsr3_spmv(const rk_csr A, const double* __restrict__ x,
                                                             double* __restrict__ y) {
   const int lane = threadIdx.x & 31;
   const int64_t nbr = A.n / 3;
@@ -390,7 +450,7 @@ __global__ void __launch_bounds__(kSpmvThreads) k_bsr3_spmv(const rk_csr A, cons
   const int64_t wpb = kSpmvThreads / 32;
   for (int64_t sl = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); sl < nsl; sl += (int64_t)gridDim.x * wpb) {
     double s0, s1, s2;
-    sell3_row<2>(A, x, sl, lane, s0, s1, s2);
+    sell3_row<3>(A, x, sl, lane, s0, s1, s2);
     const int64_t br = sl * 32 + lane;
     if (br < nbr) {
       y[3 * br] = s0;
@@ -401,7 +461,7 @@ __global__ void __launch_bounds__(kSpmvThreads) k_bsr3_spmv(const rk_csr A, cons
 }
 
 template <int U>
-__global__ void __launch_bounds__(kSpmvThreads) k_bsr3_spmv_pcg(const rk_pcg_plan P) {
+__global__ void __launch_bounds__(kSpmvThreads, (U == 14 || U == 4 || U == 3) ? 2 : (U == 5 ? 3 : 1)) k_bsr3_spmv_pcg(const rk_pcg_plan P) {
   pdl_wait();
   pdl_trigger();
   if (P.st->done) return;
@@ -417,6 +477,8 @@ __global__ void __launch_bounds__(kSpmvThreads) k_bsr3_spmv_pcg(const rk_pcg_pla
   for (int64_t sl = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); sl < nsl; sl += (int64_t)gridDim.x * wpb) {
     double s0, s1, s2;
     if constexpr (U == 0) sell3_row_pipe(P.A, p, sl, lane, s0, s1, s2);
+    else if constexpr (U >= 12) sell3_row_issue<U - 10>(P.A, p, sl, lane, s0, s1, s2);
+    else if constexpr (U == 5) sell3_row<4>(P.A, p, sl, lane, s0, s1, s2);
     else sell3_row<U>(P.A, p, sl, lane, s0, s1, s2);
     const int64_t br = sl * 32 + lane;
     if (br < nbr) {
@@ -550,10 +612,13 @@ static void launch_bsr3_spmv_pcg_u(const rk_pcg_plan& P, cudaStream_t s) {
 static int sell_unroll() {
   static const int v = [] {
     const char* e = getenv("RK_SELL_U");
-    // 2 slot rows in flight (default); 0 = two-stage software pipeline (3% faster
-    // in isolation, equal inside the sequence, and 128 registers)
-    const int x = e ? atoi(e) : 2;
-    return (x >= 0 && x <= 4) ? x : 2;
+    // 3 slot rows in flight with room for 110 registers (2 blocks/SM), so every
+    // column and value load of the 3 rows is issued before the first gather:
+    // measured 94.6 us vs 98.5 us for 2 rows at 48 registers (C3). Others are
+    // kept for measurement: 0 = two-stage software pipeline, 12/14 = explicit
+    // issue order with 2/4 rows, 5 = 4 rows at 3 blocks/SM.
+    const int x = e ? atoi(e) : 3;
+    return ((x >= 0 && x <= 5) || x == 12 || x == 14) ? x : 3;
   }();
   return v;
 }
@@ -562,9 +627,12 @@ static void launch_bsr3_spmv_pcg(const rk_pcg_plan& P, cudaStream_t s) {
   switch (sell_unroll()) {
     case 0: launch_bsr3_spmv_pcg_u<0>(P, s); break;
     case 1: launch_bsr3_spmv_pcg_u<1>(P, s); break;
-    case 3: launch_bsr3_spmv_pcg_u<3>(P, s); break;
     case 4: launch_bsr3_spmv_pcg_u<4>(P, s); break;
-    default: launch_bsr3_spmv_pcg_u<2>(P, s); break;
+    case 5: launch_bsr3_spmv_pcg_u<5>(P, s); break;
+    case 12: launch_bsr3_spmv_pcg_u<12>(P, s); break;  // volatile-issue variants: 2 / 4 slot rows
+    case 14: launch_bsr3_spmv_pcg_u<14>(P, s); break;
+    case 2: launch_bsr3_spmv_pcg_u<2>(P, s); break;
+    default: launch_bsr3_spmv_pcg_u<3>(P, s); break;
   }
 }
 
