@@ -58,6 +58,14 @@ constexpr int kProjChunk = 1024;                 // rows per update block
 constexpr int kProjCols = 32;                    // cross columns per update block (4 per warp)
 constexpr int kMaxProj = 2048;                   // projection width of the fused path
 constexpr int kStageFactor = 96;                 // Linv staged in shared memory up to this width
+#ifndef RK_DIR_UNROLL
+#define RK_DIR_UNROLL 12
+#endif
+#ifndef RK_DIR_MINB
+#define RK_DIR_MINB 4
+#endif
+constexpr int kDirUnroll = RK_DIR_UNROLL;          // B loads in flight per row in the direction kernel
+constexpr int kDirMinBlocks = RK_DIR_MINB;
 constexpr int kFuseMax = 64;                     // widths whose finish runs in the update kernel's tail
 constexpr int kMaxGroups = 256;                  // chunk groups of the fused two-level combine
 
@@ -455,7 +463,7 @@ __global__ void __launch_bounds__(256) k_pcg_finish(const rk_pcg_plan P, int ent
 }
 
 // K5: new direction into V[:, k+1] (entry: V[:, 0]).
-__global__ void __launch_bounds__(256) k_pcg_direction(const rk_pcg_plan P, int entry) {
+__global__ void __launch_bounds__(256, kDirMinBlocks) k_pcg_direction(const rk_pcg_plan P, int entry) {
   rk_pcg_state* st = P.st;
   pdl_wait();
   pdl_trigger();
@@ -486,13 +494,13 @@ __global__ void __launch_bounds__(256) k_pcg_direction(const rk_pcg_plan P, int 
       double s = 0.0;
       const double* row = B + i;
       int64_t j = 0;
-      for (; j + 4 <= m; j += 4) {
-        const double b0 = __ldcs(row + (j + 0) * P.ldb), b1 = __ldcs(row + (j + 1) * P.ldb);
-        const double b2 = __ldcs(row + (j + 2) * P.ldb), b3 = __ldcs(row + (j + 3) * P.ldb);
-        s = fma(b0, mus[j], s);
-        s = fma(b1, mus[j + 1], s);
-        s = fma(b2, mus[j + 2], s);
-        s = fma(b3, mus[j + 3], s);
+      // kDirUnroll loads of B issued before their fmas (same j order)
+      for (; j + kDirUnroll <= m; j += kDirUnroll) {
+        double b[kDirUnroll];
+#pragma unroll
+        for (int u = 0; u < kDirUnroll; ++u) b[u] = __ldcs(row + (j + u) * P.ldb);
+#pragma unroll
+        for (int u = 0; u < kDirUnroll; ++u) s = fma(b[u], mus[j + u], s);
       }
       for (; j < m; ++j) s = fma(__ldcs(row + j * P.ldb), mus[j], s);
       t = __dsub_rn(t, s);
