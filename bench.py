@@ -263,7 +263,7 @@ def run_b200(args, rank, world, dist):
     A0 = dev_specs[0].A
     if A0.bval is not None:
         bsr = A0._pattern.bsr
-        fmt = (f"SELL-32 of 3x3 blocks (SoA fp64 values, int32 block columns; {bsr.nblk} slots for "
+        fmt = (f"SELL-32 of 3x3 blocks (9x32 fp64 value tiles per slot row, int32 block columns; {bsr.nblk} slots for "
                f"{bsr.nreal} blocks, {100.0 * (bsr.nblk - bsr.nreal) / bsr.nblk:.1f}% padding)")
         alg_bytes = bsr3_bytes(n, bsr.nblk)
     else:
@@ -276,6 +276,7 @@ def run_b200(args, rank, world, dist):
             traffic = json.load(fh).get("k_spmv_pcg", {}).get("dram_bytes_per_launch")
     except Exception:
         pass
+    gram = _gram_roofline(dev_specs[0].A, reports)
     iters = [r.stage3_iters for r in reports]
     sched = {"stage3_iters": iters, "truncated": [bool(r.truncated) for r in reports],
              "basis_dim": [r.basis_dim for r in reports], "grown": [r.basis_dim + r.stage3_iters for r in reports]}
@@ -307,6 +308,7 @@ def run_b200(args, rank, world, dist):
             "avg_launch_ms": round(avg[0], 4),
             "peak_source": peaks["source"],
         },
+        "gram": gram,
         "kernels_ms_avg": {"spmv_pcg": round(avg[0], 4), "pcg_update": round(avg[1], 4),
                            "pcg_finish": round(avg[2], 4), "pcg_direction": round(avg[3], 4),
                            "launches": list(cnt)},
@@ -324,6 +326,47 @@ def run_b200(args, rank, world, dist):
         with open(os.path.join(ROOT, "gpurun_out", "c3_schedule.json"), "w") as fh:
             json.dump(sched, fh)
     return line, host_specs, sched
+
+
+DMMA_PEAK_TFLOPS = 37.1  # B200 FP64 tensor (DMMA) peak measured by scripts/dmma_probe.cu (profiles/dmma_peak_r01.json)
+
+
+def _gram_roofline(A, reports):
+    """BASELINE's second metric: the truncation Gram Z'AZ (rk_gram_upper from
+    cached products, DMMA) at the sequence's own truncation width, timed with
+    CUDA events after the timed region (3 launches, random data of that shape),
+    against the measured DMMA peak. Flops counted for the upper triangle only,
+    N m (m + 1)."""
+    import torch
+
+    from paper_1512_05820_b200.linalg import empty_block, symmetric_gram_from_products
+
+    grown = [r.basis_dim + r.stage3_iters for r in reports if r.truncated]
+    if not grown:
+        return None
+    m = int(np.median(grown))
+    y_old = min(60, m - 1)
+    n = A.n
+    dev = A.device
+    g = torch.Generator(device=dev).manual_seed(1)
+    Z, AY, AV = empty_block(n, m, dev), empty_block(n, y_old, dev), empty_block(n, m - y_old, dev)
+    for t in (Z, AY, AV):
+        t.copy_(torch.randn(t.shape, generator=g, device=dev, dtype=torch.float64))
+    symmetric_gram_from_products(Z, [(AY, 0), (AV, y_old)])
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(3):
+        symmetric_gram_from_products(Z, [(AY, 0), (AV, y_old)])
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 3
+    tf = n * m * (m + 1) / (ms * 1e-3) / 1e12
+    del Z, AY, AV
+    return {"kernel": "K7 k_gram (rk_gram_upper, DMMA m8n8k4 f64)", "bound": "tensor", "n": n, "m": m,
+            "ms": round(ms, 3), "achieved": round(tf, 2), "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "frac": round(tf / DMMA_PEAK_TFLOPS, 3),
+            "peak_source": "measured DMMA register-only probe (scripts/dmma_probe.cu); cuBLAS DGEMM 35.5"}
 
 
 def _peaks():
