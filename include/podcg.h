@@ -218,6 +218,14 @@ int rk_gram(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m2,
 int rk_gram_upper(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m2,
                   const double* Y, int64_t ldy, int64_t col_off, double* G, int64_t ldg,
                   double* ws, int64_t ws_len, void* stream);
+/* The whole snapshot Gram Z'AZ (m x m, upper triangle, col_off 0) when A Z is
+ * held as two column segments: columns [0, c1) of AZ in Y1 (the stage-1 product
+ * A W), columns [c1, m) in Y2 (the A p_k the PCG run stored). One launch with
+ * tiles aligned to the diagonal (pod.py:119 `S.T @ AS` on the grown block,
+ * threestage.py:510-524). ws: rk_gram_upper_workspace_doubles(n, m, m, 0). */
+int rk_gram_upper_split(int64_t n, int64_t m, const double* X, int64_t ldx, int64_t c1,
+                        const double* Y1, int64_t ldy1, const double* Y2, int64_t ldy2,
+                        double* G, int64_t ldg, double* ws, int64_t ws_len, void* stream);
 /* Out (N x y) = S (N x s) C (s x y) (pod.py:91-93 `S @ coef`). */
 int rk_gemm_nn(int64_t n, int64_t s, int64_t y, const double* S, int64_t lds,
                const double* C, int64_t ldc, double* Out, int64_t ldo, void* stream);

@@ -114,7 +114,8 @@ void launch_scale_columns(int64_t n, int64_t m, const double* V, int64_t ldv, co
 void launch_axpby(int64_t n, double a, const double* x, double b, double* y, cudaStream_t s);
 void launch_sub_from(int64_t n, const double* x0, double* y, cudaStream_t s);
 int launch_gram(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m2, const double* Y, int64_t ldy,
-                double* G, int64_t ldg, double* ws, int64_t ws_len, int64_t upper_off, cudaStream_t s);
+                const double* Y2, int64_t ldy2, int64_t c1, double* G, int64_t ldg, double* ws, int64_t ws_len,
+                int64_t upper_off, cudaStream_t s);
 int64_t gram_workspace_doubles(int64_t n, int64_t m1, int64_t m2, int64_t upper_off);
 int debug_trace(unsigned long long* out, int64_t n);
 int launch_gemm_nn(int64_t n, int64_t sdim, int64_t y, const double* S, int64_t lds, const double* C, int64_t ldc,
@@ -297,14 +298,24 @@ int rk_gram(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m2, con
                  "rk_gram: memset failed");
     return RK_OK;
   }
-  return rkh::launch_gram(n, m1, X, ldx, m2, Y, ldy, G, ldg, ws, ws_len, -1, as_stream(stream));
+  return rkh::launch_gram(n, m1, X, ldx, m2, Y, ldy, nullptr, 0, m2, G, ldg, ws, ws_len, -1, as_stream(stream));
 }
 
 int rk_gram_upper(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m2, const double* Y, int64_t ldy,
                   int64_t col_off, double* G, int64_t ldg, double* ws, int64_t ws_len, void* stream) {
   RK_REQUIRE(n >= 0 && m1 >= 0 && m2 >= 0 && col_off >= 0, RK_ERR_DIMENSION, "rk_gram_upper: bad shape");
   if (n == 0) return rk_gram(n, m1, X, ldx, m2, Y, ldy, G, ldg, ws, ws_len, stream);
-  return rkh::launch_gram(n, m1, X, ldx, m2, Y, ldy, G, ldg, ws, ws_len, col_off, as_stream(stream));
+  return rkh::launch_gram(n, m1, X, ldx, m2, Y, ldy, nullptr, 0, m2, G, ldg, ws, ws_len, col_off, as_stream(stream));
+}
+
+int rk_gram_upper_split(int64_t n, int64_t m, const double* X, int64_t ldx, int64_t c1, const double* Y1, int64_t ldy1,
+                        const double* Y2, int64_t ldy2, double* G, int64_t ldg, double* ws, int64_t ws_len,
+                        void* stream) {
+  RK_REQUIRE(n >= 0 && m >= 0 && c1 >= 0 && c1 <= m, RK_ERR_DIMENSION, "rk_gram_upper_split: bad shape");
+  RK_REQUIRE(c1 == m || Y2 != nullptr, RK_ERR_ARG, "rk_gram_upper_split: second segment missing");
+  if (n == 0) return rk_gram(n, m, X, ldx, m, Y1, ldy1, G, ldg, ws, ws_len, stream);
+  return rkh::launch_gram(n, m, X, ldx, m, c1 > 0 ? Y1 : Y2, c1 > 0 ? ldy1 : ldy2, Y2, ldy2, c1, G, ldg, ws, ws_len,
+                          0, as_stream(stream));
 }
 
 int rk_gemm_nn(int64_t n, int64_t s, int64_t y, const double* S, int64_t lds, const double* C, int64_t ldc,

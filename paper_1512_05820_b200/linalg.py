@@ -548,7 +548,7 @@ class UpperGram:
     """Symmetric Gram Z'AZ kept on the device as its upper triangle.
 
     ``store`` is an (m, m) tensor read as a column-major matrix (ld = m) whose
-    upper 64x64 tiles were produced by rk_gram_upper; ``scale`` (device vector
+    upper tiles were produced by rk_gram_upper(_split); ``scale`` (device vector
     or None) multiplies column b of the triangle. ``np.asarray`` gives the full
     mirrored host matrix (the reference's ``gram_zz``)."""
 
@@ -570,12 +570,13 @@ class UpperGram:
         return (self.m, self.m)
 
 
-def symmetric_gram_from_products(Z: torch.Tensor, products, col_scale=None) -> UpperGram:
+def symmetric_gram_from_products(Z: torch.Tensor, products, col_scale=None, single_launch: bool = True) -> UpperGram:
     """Z'AZ from cached products A Z (no SpMM).
 
     ``products`` is a list of (AZ_block, col_off): AZ_block holds A applied to
     columns [col_off, col_off + w) of Z (the stage-1 product A W and the stored
-    A p_k of the PCG run). Only the upper 64x64 tiles are computed
+    A p_k of the PCG run); two contiguous segments covering Z go to one
+    rk_gram_upper_split launch. Only the upper tiles are computed
     (rk_gram_upper, half the flops of the reference's full B'(AB));
     ``col_scale`` (length m or None) rescales column j (products of unscaled
     directions)."""
@@ -583,6 +584,20 @@ def symmetric_gram_from_products(Z: torch.Tensor, products, col_scale=None) -> U
     dev = Z.device
     store = torch.zeros((max(m, 1), max(m, 1)), dtype=F64, device=dev)  # column-major m x m (ld = m)
     s = nat.scratch(dev)
+    scale = as_vector(col_scale, dev) if col_scale is not None else None
+    segs = [(AB, off) for AB, off in products if int(AB.shape[1])]
+    if single_launch and len(segs) <= 2 and segs and segs[0][1] == 0 and sum(int(AB.shape[1]) for AB, _ in segs) == m and \
+            (len(segs) == 1 or segs[1][1] == int(segs[0][0].shape[1])):
+        # A Z covered by at most two contiguous segments: one launch whose tiles
+        # sit on the diagonal of the whole m x m triangle
+        Y1 = segs[0][0]
+        Y2 = segs[1][0] if len(segs) == 2 else Y1
+        c1 = int(Y1.shape[1])
+        ws = s.workspace(max(nat.lib().rk_gram_upper_workspace_doubles(n, m, m, 0), 1))
+        nat.check(nat.lib().rk_gram_upper_split(n, m, Z.data_ptr(), block_ld(Z), c1, Y1.data_ptr(), block_ld(Y1),
+                                                Y2.data_ptr(), block_ld(Y2), store.data_ptr(), m, ws.data_ptr(),
+                                                ws.numel(), nat.stream_ptr(dev)), "gram_upper_split")
+        return UpperGram(store[:m, :m], scale)
     for AB, off in products:
         w = int(AB.shape[1])
         if w == 0:
@@ -592,7 +607,6 @@ def symmetric_gram_from_products(Z: torch.Tensor, products, col_scale=None) -> U
         nat.check(nat.lib().rk_gram_upper(n, m, Z.data_ptr(), block_ld(Z), w, AB.data_ptr(), block_ld(AB), off,
                                           Gblk.data_ptr(), m, ws.data_ptr(), ws.numel(), nat.stream_ptr(dev)),
                   "gram_upper")
-    scale = as_vector(col_scale, dev) if col_scale is not None else None
     return UpperGram(store[:m, :m], scale)
 
 
