@@ -42,7 +42,6 @@ warnings.simplefilter("ignore")
 
 METRIC = "sequence solve time"
 UNIT = "s"
-SCHEDULE = os.path.join(ROOT, "profiles", "c3_schedule.json")
 NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
 
 
@@ -57,27 +56,61 @@ def parse():
     ap.add_argument("--grid", type=int, default=64)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--workload", default="c3", choices=["c3", "c2", "c5"],
+                    help="c3 (default, the north-star sequence), c2 (128^3 diffusion sequence), "
+                         "c5 (POD truncation microbench)")
+    ap.add_argument("--m", type=int, default=2048, help="c5: snapshot columns")
+    args = ap.parse_args()
+    if args.workload == "c2" and args.systems == 40:
+        args.systems = 30
+    return args
+
+
+# BASELINE configs[1] (C2) and configs[2] (C3): sequence workloads
+WORKLOADS = {
+    "c3": {"rtol": 1e-5, "cap": 60, "data": "synthetic (seeded C3 generator, BASELINE configs[2] shapes)",
+           "l2": "inputs larger than L2 (552 MB of 3x3-block matrix streamed per SpMV, 20 GB of matrices); no flush"},
+    "c2": {"rtol": 1e-4, "cap": 40, "data": "synthetic (seeded C2 generator, BASELINE configs[1] shapes)",
+           "l2": "inputs larger than L2 (175 MB of CSR streamed per SpMV, 3.5 GB of matrices); no flush"},
+}
+
+
+def make_sequence(args, seed_offset=0, p=None):
+    from paper_1512_05820_b200.problems import diffusion3d_sequence, elasticity_sequence
+
+    p = args.systems if p is None else p
+    if args.workload == "c2":
+        return diffusion3d_sequence(128, p=p, rtol=1e-4, seed=2 + seed_offset)
+    return elasticity_sequence((args.grid,) * 3, p=p, rtol=1e-5, seed=3 + seed_offset)
 
 
 def workload_config(args, n=None, nnz=None):
+    w = WORKLOADS[args.workload]
+    name = (f"C2 variable-coefficient diffusion 128^3, {args.systems}-system recycled sequence"
+            if args.workload == "c2" else
+            f"C3 Q1 elasticity {args.grid}^3 elements, {args.systems}-system recycled sequence")
     return {
-        "workload": f"C3 Q1 elasticity {args.grid}^3 elements, {args.systems}-system recycled sequence",
+        "workload": name,
         "systems": args.systems,
         "n": n,
         "nnz": nnz,
         "mode": args.mode,
         "preconditioner": "jacobi",
-        "rtol": 1e-5,
-        "truncation": "pod-a-rbf nu_y=1 nu_w=1 storage_cap=60 max_dim=60",
-        "l2": "inputs larger than L2 (552 MB of 3x3-block matrix streamed per SpMV, 20 GB of matrices); no flush",
+        "rtol": w["rtol"],
+        "truncation": f"pod-a-rbf nu_y=1 nu_w=1 storage_cap={w['cap']} max_dim={w['cap']}",
+        "l2": w["l2"],
         "parallelism": "replicas (one independent sequence per GPU)",
     }
 
 
-def solver_config(pk, mode):
-    tr = pk.TruncationConfig(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=60, max_dim=60)
-    return pk.SolverConfig(truncation=tr, mode=mode)
+def solver_config(pk, args):
+    cap = WORKLOADS[args.workload]["cap"]
+    tr = pk.TruncationConfig(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=cap, max_dim=cap)
+    return pk.SolverConfig(truncation=tr, mode=args.mode)
+
+
+def schedule_path(args):
+    return os.path.join(ROOT, "profiles", f"{args.workload}_schedule.json")
 
 
 # ---------------------------------------------------------------------------
@@ -188,13 +221,11 @@ def run_b200(args, rank, world, dist):
 
     import paper_1512_05820_b200 as pk
     from paper_1512_05820_b200 import _native as nat
-    from paper_1512_05820_b200.problems import elasticity_sequence
-
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     lib = nat.lib()
-    seq = elasticity_sequence((args.grid,) * 3, p=args.systems, rtol=1e-5, seed=3 + rank)
+    seq = make_sequence(args, seed_offset=rank)
     host_specs = list(seq)  # host CSR values + rhs for every system (the e2e inputs)
     n = seq.n
     nnz = host_specs[0].A.nnz
@@ -204,7 +235,7 @@ def run_b200(args, rank, world, dist):
         A = pk.SparseSpdMatrix.from_host(s.A)
         dev_specs.append(pk.LinearSystemSpec(A=A, b=torch.from_numpy(s.b).to(dev), xbar=None, tol=s.tol))
     dseq = pk.SystemSequence(n, dev_specs, C=seq.C)
-    cfg = solver_config(pk, args.mode)
+    cfg = solver_config(pk, args)
     jac = lambda A: pk.build_preconditioner("jacobi", A)  # noqa: E731
     torch.cuda.synchronize()
 
@@ -271,11 +302,12 @@ def run_b200(args, rank, world, dist):
         alg_bytes = spmv_bytes(n, nnz)
     ach = alg_bytes / (avg[0] * 1e-3) / 1e9
     traffic = None
-    try:
-        with open(NCU_SUMMARY) as fh:
-            traffic = json.load(fh).get("k_spmv_pcg", {}).get("dram_bytes_per_launch")
-    except Exception:
-        pass
+    if args.workload == "c3":  # the committed ncu capture is of the C3 SELL kernel
+        try:
+            with open(NCU_SUMMARY) as fh:
+                traffic = json.load(fh).get("k_spmv_pcg", {}).get("dram_bytes_per_launch")
+        except Exception:
+            pass
     gram = _gram_roofline(dev_specs[0].A, reports)
     iters = [r.stage3_iters for r in reports]
     sched = {"stage3_iters": iters, "truncated": [bool(r.truncated) for r in reports],
@@ -292,7 +324,7 @@ def run_b200(args, rank, world, dist):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (seeded C3 generator, BASELINE configs[2] shapes)",
+        "data": WORKLOADS[args.workload]["data"],
         "config": workload_config(args, n, nnz),
         "roofline": {
             "kernel": "K1 SpMV fused with p'Ap, p'p (k_bsr3_spmv_pcg / k_spmv_pcg)",
@@ -323,7 +355,7 @@ def run_b200(args, rank, world, dist):
         line["phases_s_per_step"] = {k: round(v / max(args.steps, 1), 4) for k, v in _timing.TIMES.items()}
     if rank == 0:
         os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-        with open(os.path.join(ROOT, "gpurun_out", "c3_schedule.json"), "w") as fh:
+        with open(os.path.join(ROOT, "gpurun_out", f"{args.workload}_schedule.json"), "w") as fh:
             json.dump(sched, fh)
     return line, host_specs, sched
 
@@ -369,6 +401,233 @@ def _gram_roofline(A, reports):
             "peak_source": "measured DMMA register-only probe (scripts/dmma_probe.cu); cuBLAS DGEMM 35.5"}
 
 
+# ---------------------------------------------------------------------------
+# C5: POD truncation microbench (BASELINE configs[4])
+# ---------------------------------------------------------------------------
+C5_GRID = (128, 128, 256)
+C5_BLOCK = 256
+
+
+def _c5_flops(n, m):
+    """Gram flops as computed: one triangle, N m (m + 1)."""
+    return float(n) * m * (m + 1)
+
+
+def run_c5(args, rank, world, dist):
+    """One step = the POD truncation of a seeded N(0,1) snapshot block S
+    (N = 4,194,304 x m) against the 7-point Laplacian on 128x128x256:
+    A S and the upper triangle of S'(AS) column block by column block
+    (assemble_gram_blocked, A S never held whole), the m x m eigenproblem
+    (cuSOLVER), Phi = S V Sigma^-1 (DMMA), plus a 20-SpMV sweep on A.
+    ``value`` = Gram flops / time of the A S + Gram phase."""
+    import torch
+
+    import paper_1512_05820_b200 as pk
+    from paper_1512_05820_b200 import _native as nat
+    from paper_1512_05820_b200.linalg import empty_block, spmv_into
+    from paper_1512_05820_b200.problems import laplacian3d
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lib = nat.lib()
+    L = laplacian3d(*C5_GRID)
+    A = pk.SparseSpdMatrix(L.n, L.row_offsets, L.col_indices, L.values)
+    n, m = L.n, args.m
+    S = empty_block(n, m, dev)
+    g = torch.Generator(device=dev).manual_seed(5 + rank)
+    for j0 in range(0, m, 128):
+        S[:, j0 : j0 + 128].normal_(generator=g)
+    gamma = np.ones(m)
+    x = S[:, 0].clone()
+    y = torch.empty_like(x)
+    torch.cuda.synchronize()
+
+    def step(events=None):
+        G = pk.assemble_gram_blocked(A, S, block=C5_BLOCK, events=events)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record()
+        res = pk.pod_evd_from_gram(G, S, gamma, 1.0)
+        e2 = torch.cuda.Event(enable_timing=True)
+        e2.record()
+        a, b = x, y
+        for _ in range(20):
+            spmv_into(A, a, b)
+            a, b = b, a
+        e3 = torch.cuda.Event(enable_timing=True)
+        e3.record()
+        return G, res, (e1, e2, e3)
+
+    for _ in range(args.warmup):
+        _, res, _ = step()
+        del res
+    torch.cuda.synchronize()
+    launches0 = lib.rk_launch_count()
+    t_gram_phase, t_pod, t_spmv, t_spmm_k, t_gram_k, t_step = [], [], [], [], [], []
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            barrier(dist)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            evs = []
+            G, res, (e1, e2, e3) = step(evs)
+            torch.cuda.synchronize()
+            t_gram_phase.append(e0.elapsed_time(e1) / 1e3)
+            t_pod.append(e1.elapsed_time(e2) / 1e3)
+            t_spmv.append(e2.elapsed_time(e3) / 1e3 / 20)
+            t_step.append(e0.elapsed_time(e3) / 1e3)
+            t_spmm_k.append(sum(a.elapsed_time(b) for a, b, _ in evs) / 1e3)
+            t_gram_k.append(sum(b.elapsed_time(c) for _, b, c in evs) / 1e3)
+            if _ < args.steps - 1:
+                del res
+    launches = (lib.rk_launch_count() - launches0) / max(args.steps, 1)
+    tg = max_over_ranks(float(np.mean(t_gram_phase)), dist)
+    flops = _c5_flops(n, m)
+    y_kept = int(res.columns.shape[1])
+    # size-independent checks (untimed): the POD basis is A-orthonormal,
+    # Phi' A Phi = Sigma^-1 V' G V Sigma^-1 = I, on its leading 32 columns
+    P = res.columns[:, :32]
+    Gp, _ = pk.assemble_gram(A, P)
+    orth = float((Gp - torch.eye(P.shape[1], dtype=torch.float64, device=dev)).abs().max())
+    sig = res.singular_values
+    e2e = None
+    if not args.no_e2e:
+        # public-API path from host memory: S H2D (pinned), the same truncation,
+        # Phi D2H; the pinned host block is reused for Phi
+        host = torch.empty((m, n), dtype=torch.float64, pin_memory=True)
+        host.copy_(S.t())
+        del res, G, P, Gp
+        torch.cuda.empty_cache()
+        torch.cuda.synchronize()
+        barrier(dist)
+        t0 = time.perf_counter()
+        S.copy_(host.t())
+        G = pk.assemble_gram_blocked(A, S, block=C5_BLOCK)
+        res = pk.pod_evd_from_gram(G, S, gamma, 1.0)
+        ph = host[: res.columns.shape[1]].t()
+        ph.copy_(res.columns)
+        torch.cuda.synchronize()
+        t_e2e = max_over_ranks(time.perf_counter() - t0, dist)
+        e2e = {"value": round(flops / t_e2e / 1e12 * world, 3), "unit": "TFLOP/s",
+               "h2d_bytes_per_step": int(n * m * 8 * world),
+               "d2h_bytes_per_step": int(n * int(res.columns.shape[1]) * 8 * world),
+               "seconds_per_step": round(t_e2e, 4),
+               "path": "S from pinned host memory -> assemble_gram_blocked -> pod_evd_from_gram -> Phi to host"}
+        del host
+    gk = float(np.mean(t_gram_k))
+    achieved = flops / gk / 1e12
+    spmv_b = spmv_bytes(n, L.nnz)
+    peaks = _peaks()
+    spmv_gbs = spmv_b / float(np.mean(t_spmv)) / 1e9
+    spmm_cols_bytes = (12 * L.nnz + 4 * (n + 1)) * math.ceil(C5_BLOCK / 8) * math.ceil(m / C5_BLOCK) + 16 * n * m
+    line = {
+        "metric": "snapshot-Gram FP64 TFLOP/s",
+        "value": round(flops / tg / 1e12 * world, 3),
+        "unit": "TFLOP/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(tg * 1e3, 2),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (S ~ N(0,1) from a seed on the device; 7-point Laplacian, BASELINE configs[4] shapes)",
+        "config": {"workload": f"C5 POD truncation, Laplacian {C5_GRID[0]}x{C5_GRID[1]}x{C5_GRID[2]}, "
+                               f"S {n} x {m}", "n": n, "nnz": L.nnz, "m": m, "column_block": C5_BLOCK,
+                   "gamma": 1, "nu": 1.0,
+                   "l2": "inputs larger than L2 (S is %.1f GB); no flush" % (n * m * 8 / 1e9),
+                   "parallelism": "replicas (one independent truncation per GPU)"},
+        "roofline": {"kernel": "K7 k_gram (rk_gram_upper per column block, DMMA m8n8k4 f64)", "bound": "tensor",
+                     "achieved": round(achieved, 2), "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": round(achieved / DMMA_PEAK_TFLOPS, 3), "traffic": None,
+                     "flops_per_step": flops, "kernel_s": round(gk, 4),
+                     "peak_source": "measured DMMA register-only probe (scripts/dmma_probe.cu); cuBLAS DGEMM 35.5"},
+        "phases_s": {"spmm_plus_gram": round(tg, 4), "spmm_kernels": round(float(np.mean(t_spmm_k)), 4),
+                     "gram_kernels": round(gk, 4), "evd_coef_reconstruction": round(float(np.mean(t_pod)), 4),
+                     "pod_truncation_total": round(float(np.mean(t_step)) - 20 * float(np.mean(t_spmv)), 4)},
+        "spmm": {"bytes_per_step": spmm_cols_bytes,
+                 "GB_s": round(spmm_cols_bytes / float(np.mean(t_spmm_k)) / 1e9, 1)},
+        "spmv": {"kernel": "rk_spmv (CSR, fp64 values, int32 columns)", "bytes": spmv_b,
+                 "avg_ms": round(float(np.mean(t_spmv)) * 1e3, 4), "GB_s": round(spmv_gbs, 1),
+                 "frac": round(spmv_gbs / peaks["hbm_gbs"], 3), "peak": peaks["hbm_gbs"]},
+        "pod": {"y": y_kept, "sigma_1": float(sig[0]), "sigma_m": float(sig[-1]),
+                "phi_A_orthonormality_maxdev_32": orth},
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+    }
+    return line
+
+
+def cpu_sample_c5(m, cols=64):
+    """The oracle's C5 operations (scipy A @ S, OpenBLAS S'(AS), LAPACK eigh,
+    S @ coef) timed on `cols` columns of S (eigh at the full m) and scaled to m
+    columns: the reference's assemble_gram computes the full m x m product."""
+    from oracle import recycle_oracle as O
+    from paper_1512_05820_b200.problems import laplacian3d
+
+    L = laplacian3d(*C5_GRID)
+    A = O.as_csr(L)
+    n = L.n
+    rng = np.random.default_rng(5)
+    S = rng.standard_normal((n, cols))
+    t0 = time.perf_counter()
+    AS = A @ S
+    t_spmm = (time.perf_counter() - t0) / cols
+    t0 = time.perf_counter()
+    _ = S.T @ AS
+    t_pair = (time.perf_counter() - t0) / (cols * cols)
+    G = rng.standard_normal((m, m))
+    G = G @ G.T
+    np.linalg.eigh(G[:64, :64])  # LAPACK / thread-pool warm-up
+    t0 = time.perf_counter()
+    np.linalg.eigh(G)
+    t_evd = time.perf_counter() - t0
+    C = rng.standard_normal((cols, cols))
+    t0 = time.perf_counter()
+    _ = S @ C
+    t_rec_pair = (time.perf_counter() - t0) / (cols * cols)
+    t_assemble = m * t_spmm + m * m * t_pair
+    return {
+        "value": round(_c5_flops(n, m) / t_assemble / 1e12, 4),
+        "unit": "TFLOP/s",
+        "cores": len(os.sched_getaffinity(0)),
+        "kind": "port",
+        "sample": (f"oracle ops on {cols} columns of S (N = {n}): A@S {t_spmm*1e3:.1f} ms/column, S'(AS) "
+                   f"{t_pair*1e6:.1f} us per column pair, eigh({m}) {t_evd:.2f} s; scaled to m = {m} "
+                   "(full m x m product as the reference computes it; extrapolated)"),
+        "seconds": {"assemble_gram": round(t_assemble, 2), "eigh": round(t_evd, 2),
+                    "reconstruction": round(m * m * t_rec_pair, 2),
+                    "pod_truncation_total": round(t_assemble + t_evd + m * m * t_rec_pair, 2)},
+    }
+
+
+def run_reference_c5(args, world):
+    vals, cb = [], None
+    for _ in range(args.warmup):
+        cpu_sample_c5(args.m)
+    for _ in range(args.steps):
+        cb = cpu_sample_c5(args.m)
+        vals.append(cb["value"])
+    v = float(np.mean(vals))
+    cb["value"] = round(v, 4)
+    n = C5_GRID[0] * C5_GRID[1] * C5_GRID[2]
+    return {
+        "impl": "reference", "metric": "snapshot-Gram FP64 TFLOP/s", "value": round(v, 4), "unit": "TFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (S ~ N(0,1) from a seed; 7-point Laplacian, BASELINE configs[4] shapes)",
+        "config": {"workload": f"C5 POD truncation, Laplacian {C5_GRID[0]}x{C5_GRID[1]}x{C5_GRID[2]}, "
+                               f"S {n} x {args.m}", "n": n, "m": args.m},
+        "cpu_baseline": cb,
+        "e2e": {"value": round(v, 4), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference = numpy/scipy (recykl); its operations timed through oracle/recycle_oracle.py on a "
+                "bounded sample and scaled to m columns (extrapolated)",
+    }
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -381,9 +640,9 @@ def _peaks():
 # ---------------------------------------------------------------------------
 # CPU oracle sample, scaled to the metric
 # ---------------------------------------------------------------------------
-def cpu_sample(host_specs, sched, budget_s=20.0):
+def cpu_sample(host_specs, sched, cap=60, label="C3", budget_s=20.0):
     """Time the oracle (numpy/scipy, as the reference) on a bounded sample of
-    the C3 workload and scale it to one sequence with the GPU run's schedule:
+    the sequence workload and scale it to one sequence with the GPU run's schedule:
     t = sum_j iters_j * t_iter(m_j) + sum_truncations t_trunc(grown_j)."""
     import scipy.sparse  # noqa: F401
 
@@ -413,7 +672,7 @@ def cpu_sample(host_specs, sched, budget_s=20.0):
 
     k0 = 12
     t_it0 = iters_cost(None, k0)
-    Y = np.linalg.qr(rng.standard_normal((n, 60)))[0]
+    Y = np.linalg.qr(rng.standard_normal((n, cap)))[0]
     t_it60 = iters_cost(Y, 8)
     # truncation sample: SpMM + Gram with 32 columns, eigh at full width, S @ coef sample
     s_cols = 32
@@ -439,15 +698,16 @@ def cpu_sample(host_specs, sched, budget_s=20.0):
         for j, (k, g) in enumerate(zip(sched["stage3_iters"], sched["grown"])):
             total += k * (t_it0 if j == 0 else t_it60)
             if j > 0:
-                total += 60 * t_spmm + 60 * 60 * t_gram_unit      # stage-1 assemble_gram of W
-            total += g * t_spmm + g * g * t_gram_unit + t_evd * (g / grown) ** 3 + g * t_rec_unit
+                total += cap * t_spmm + cap * cap * t_gram_unit   # stage-1 assemble_gram of W
+            if g > cap:  # truncation: SpMM + Gram of the grown block, eigh, reconstruction
+                total += g * t_spmm + g * g * t_gram_unit + t_evd * (g / grown) ** 3 + g * t_rec_unit
     return {
         "value": round(total, 2),
         "unit": UNIT,
         "cores": cores,
         "kind": "port",
-        "sample": (f"oracle on C3 system 1: {k0} plain PCG iterations ({t_it0*1e3:.0f} ms/it), 8 iterations "
-                   f"projected against 60 columns ({t_it60*1e3:.0f} ms/it), a {s_cols}-column SpMM+Gram, "
+        "sample": (f"oracle on {label} system 1: {k0} plain PCG iterations ({t_it0*1e3:.0f} ms/it), 8 iterations "
+                   f"projected against {cap} columns ({t_it60*1e3:.0f} ms/it), a {s_cols}-column SpMM+Gram, "
                    f"S@coef and eigh({grown}); scaled to the sequence with the GPU run's schedule "
                    f"({sum(sched['stage3_iters']) if sched else 0} stage-3 iterations, extrapolated)"),
         "components_s": {"t_iter_plain": t_it0, "t_iter_m60": t_it60, "t_spmm_per_col": t_spmm,
@@ -459,21 +719,22 @@ def run_reference(args, rank, world):
     """--impl reference: the oracle port on the box's host cores (rank 0 only)."""
     if rank != 0:
         return None
-    from paper_1512_05820_b200.problems import elasticity_sequence
-
-    seq = elasticity_sequence((args.grid,) * 3, p=min(args.systems, 1), rtol=1e-5, seed=3)
+    if args.workload == "c5":
+        return run_reference_c5(args, world)
+    seq = make_sequence(args, p=1)
     host_specs = list(seq)
-    sched = None
     try:
-        with open(SCHEDULE) as fh:
+        with open(schedule_path(args)) as fh:
             sched = json.load(fh)
     except Exception:
         sched = None
+    cap = WORKLOADS[args.workload]["cap"]
+    label = args.workload.upper()
     vals = []
     for _ in range(args.warmup):
-        cpu_sample(host_specs, sched)
+        cpu_sample(host_specs, sched, cap, label)
     for _ in range(args.steps):
-        cb = cpu_sample(host_specs, sched)
+        cb = cpu_sample(host_specs, sched, cap, label)
         vals.append(cb["value"])
     v = float(np.mean(vals))
     cb["value"] = round(v, 2)
@@ -489,12 +750,12 @@ def run_reference(args, rank, world):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (seeded C3 generator, BASELINE configs[2] shapes)",
+        "data": WORKLOADS[args.workload]["data"],
         "config": workload_config(args, seq.n, host_specs[0].A.nnz),
         "cpu_baseline": cb,
         "e2e": {"value": round(v, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": ("reference = pure-Python numpy/scipy (recykl); timed through its restatement oracle/recycle_oracle.py "
-                 "on a bounded sample and scaled with profiles/c3_schedule.json (extrapolated)"),
+                 f"on a bounded sample and scaled with profiles/{args.workload}_schedule.json (extrapolated)"),
     }
     return line
 
@@ -509,10 +770,20 @@ def main():
         if dist is not None:
             dist.destroy_process_group()
         return
+    if args.workload == "c5":
+        line = run_c5(args, rank, world, dist)
+        if rank == 0:
+            if world == 1 and not args.no_cpu:
+                line["cpu_baseline"] = cpu_sample_c5(args.m)
+            print(json.dumps(line))
+        if dist is not None:
+            dist.destroy_process_group()
+        return
     line, host_specs, sched = run_b200(args, rank, world, dist)
     if rank == 0:
         if world == 1 and not args.no_cpu:
-            line["cpu_baseline"] = cpu_sample(host_specs, sched)
+            line["cpu_baseline"] = cpu_sample(host_specs, sched, WORKLOADS[args.workload]["cap"],
+                                              args.workload.upper())
         print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()
