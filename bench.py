@@ -292,7 +292,12 @@ def run_b200(args, rank, world, dist):
     avg = [ms[i] / max(cnt[i], 1) for i in range(4)]
     peaks = _peaks()
     A0 = dev_specs[0].A
-    if A0.bval is not None:
+    if A0.bval is not None and A0.csr.bdim == 1:
+        sell = A0._pattern.sell
+        fmt = (f"scalar SELL-32 (one row per lane, fp64 values, int32 columns; {sell.nslot} slots for {nnz} "
+               f"nonzeros, {100.0 * (sell.nslot - nnz) / sell.nslot:.1f}% padding)")
+        alg_bytes = 12 * sell.nslot + 4 * ((n + 31) // 32 + 1) + 16 * n
+    elif A0.bval is not None:
         bsr = A0._pattern.bsr
         fmt = (f"SELL-32 of 3x3 blocks (9x32 fp64 value tiles per slot row, int32 block columns; {bsr.nblk} slots for "
                f"{bsr.nreal} blocks, {100.0 * (bsr.nblk - bsr.nreal) / bsr.nblk:.1f}% padding)")
@@ -518,6 +523,8 @@ def run_c5(args, rank, world, dist):
     gk = float(np.mean(t_gram_k))
     achieved = flops / gk / 1e12
     spmv_b = spmv_bytes(n, L.nnz)
+    if A.csr.bdim == 1:  # bytes of the format actually streamed (scalar SELL-32: no row pointers, padded slots)
+        spmv_b = 12 * A._pattern.sell.nslot + 4 * ((n + 31) // 32 + 1) + 16 * n
     peaks = _peaks()
     spmv_gbs = spmv_b / float(np.mean(t_spmv)) / 1e9
     spmm_cols_bytes = (12 * L.nnz + 4 * (n + 1)) * math.ceil(C5_BLOCK / 8) * math.ceil(m / C5_BLOCK) + 16 * n * m
@@ -549,7 +556,7 @@ def run_c5(args, rank, world, dist):
                      "pod_truncation_total": round(float(np.mean(t_step)) - 20 * float(np.mean(t_spmv)), 4)},
         "spmm": {"bytes_per_step": spmm_cols_bytes,
                  "GB_s": round(spmm_cols_bytes / float(np.mean(t_spmm_k)) / 1e9, 1)},
-        "spmv": {"kernel": "rk_spmv (CSR, fp64 values, int32 columns)", "bytes": spmv_b,
+        "spmv": {"kernel": "rk_spmv (%s)" % ("scalar SELL-32 view" if A.csr.bdim == 1 else "CSR"), "bytes": spmv_b,
                  "avg_ms": round(float(np.mean(t_spmv)) * 1e3, 4), "GB_s": round(spmv_gbs, 1),
                  "frac": round(spmv_gbs / peaks["hbm_gbs"], 3), "peak": peaks["hbm_gbs"]},
         "pod": {"y": y_kept, "sigma_1": float(sig[0]), "sigma_m": float(sig[-1]),

@@ -50,7 +50,7 @@ typedef struct rk_csr {
   const int32_t* col;    /* nnz, sorted within each row */
   const double* val;     /* nnz */
   int32_t lanes;         /* lanes cooperating on one row: 1,2,4,8,16,32 (0 = auto) */
-  int32_t pad_;
+  int32_t bdim;          /* block size of the sliced-ELL view below: 0 or 3 = 3x3 blocks, 1 = scalar */
   /* Optional sliced-ELL view of the same matrix in 3x3 blocks (vector-valued
    * problems such as the Q1 elasticity operator; SELL-32: 32 block rows per
    * slice, padded to the slice's widest row). When bval != NULL the SpMV
@@ -59,7 +59,11 @@ typedef struct rk_csr {
    * Slot (slice s, position t, lane l) = browptr[s] + 32 t + l. Values come
    * in one contiguous 9 x 32 tile per slot row: entry e = 3*a + c (row a,
    * column c) of the block in slot q is bval[9 * (q - q % 32) + 32 e + q % 32]
-   * (0 for padding); rk_bsr3_gather fills them from val. */
+   * (0 for padding); rk_bsr3_gather fills them from val.
+   * With bdim == 1 the same fields hold a scalar SELL-32 view for short
+   * uniform rows (7-point stencils): browptr has ceil(n/32) + 1 slice offsets,
+   * slot (s, t, l) = browptr[s] + 32 t + l holds one column in bcol and one
+   * value in bval (12 bytes per slot), filled by rk_sell_gather. */
   int64_t nblk;           /* number of slots (stored blocks + padding) */
   const int32_t* browptr; /* ceil(n/96) + 1 slice offsets, in slots */
   const int32_t* bcol;    /* nblk block columns (padding: a valid column) */
@@ -178,6 +182,9 @@ int rk_ssor_apply(const rk_csr* A, const double* dw, const double* d, const doub
  * 3x3-block slot values of a matrix whose pattern (and perm) was built once
  * for the sequence. */
 int rk_bsr3_gather(int64_t nblk, const int32_t* perm, const double* val, double* bval, void* stream);
+/* out[s] = perm[s] >= 0 ? val[perm[s]] : 0 for s < total (the scalar SELL-32
+ * values of a new matrix on a known pattern). */
+int rk_sell_gather(int64_t total, const int32_t* perm, const double* val, double* out, void* stream);
 /* Largest |A_ij - A_ji| over stored entries and max|A_ij| (device doubles [2]);
  * replaces the scipy transpose difference of SparseSpdMatrix._validate
  * (linalg.py:105-113). Requires sorted columns. */

@@ -35,7 +35,7 @@ class RkCsr(ctypes.Structure):
         ("col", c_vp),
         ("val", c_vp),
         ("lanes", c_i32),
-        ("pad_", c_i32),
+        ("bdim", c_i32),
         ("nblk", c_i64),
         ("browptr", c_vp),
         ("bcol", c_vp),
@@ -117,6 +117,7 @@ _SIGNATURES = {
     "rk_spmm": (c_i32, [ctypes.POINTER(RkCsr), c_i64, c_vp, c_i64, c_vp, c_i64, c_vp]),
     "rk_csr_diagonal": (c_i32, [ctypes.POINTER(RkCsr), c_vp, c_vp, c_vp, c_vp]),
     "rk_csr_asymmetry": (c_i32, [ctypes.POINTER(RkCsr), c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "rk_sell_gather": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp]),
     "rk_bsr3_gather": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp]),
     "rk_gemv_t": (c_i32, [c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "rk_gemv_n": (c_i32, [c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_i32, c_vp]),

@@ -128,12 +128,16 @@ static int check_csr(const rk_csr* A) {
   RK_REQUIRE(A->lanes == 0 || A->lanes == 1 || A->lanes == 2 || A->lanes == 4 || A->lanes == 8 ||
                  A->lanes == 16 || A->lanes == 32,
              RK_ERR_ARG, "CSR: lanes must be 0 or a power of two <= 32");
-  RK_REQUIRE(!A->bval || (A->browptr && A->bcol && A->n % 3 == 0 && A->nblk * 9 >= A->nnz), RK_ERR_ARG,
-             "CSR: inconsistent 3x3 block view");
+  RK_REQUIRE(A->bdim == 0 || A->bdim == 1 || A->bdim == 3, RK_ERR_ARG, "CSR: bdim must be 0, 1 or 3");
+  RK_REQUIRE(!A->bval || A->bdim == 1 || (A->browptr && A->bcol && A->n % 3 == 0 && A->nblk * 9 >= A->nnz),
+             RK_ERR_ARG, "CSR: inconsistent 3x3 block view");
+  RK_REQUIRE(!A->bval || A->bdim != 1 || (A->browptr && A->bcol && A->nblk >= A->nnz), RK_ERR_ARG,
+             "CSR: inconsistent sliced-ELL view");
   return RK_OK;
 }
 
 int launch_bsr3_gather(int64_t nblk, const int32_t* perm, const double* val, double* bval, cudaStream_t s);
+int launch_sell_gather(int64_t total, const int32_t* perm, const double* val, double* out, cudaStream_t s);
 
 }  // namespace rkh
 
@@ -225,6 +229,12 @@ int rk_bsr3_gather(int64_t nblk, const int32_t* perm, const double* val, double*
   RK_REQUIRE(nblk >= 0, RK_ERR_DIMENSION, "rk_bsr3_gather: bad size");
   RK_REQUIRE(nblk == 0 || (perm && val && bval), RK_ERR_ARG, "rk_bsr3_gather: null pointer");
   return rkh::launch_bsr3_gather(nblk, perm, val, bval, as_stream(stream));
+}
+
+int rk_sell_gather(int64_t total, const int32_t* perm, const double* val, double* out, void* stream) {
+  RK_REQUIRE(total >= 0, RK_ERR_DIMENSION, "rk_sell_gather: bad size");
+  RK_REQUIRE(total == 0 || (perm && val && out), RK_ERR_ARG, "rk_sell_gather: null pointer");
+  return rkh::launch_sell_gather(total, perm, val, out, as_stream(stream));
 }
 
 int rk_csr_asymmetry(const rk_csr* A, double* out2, double* ws, int64_t ws_len, uint32_t* tickets, void* stream) {

@@ -559,6 +559,134 @@ __global__ void __launch_bounds__(kSpmvThreads) k_bsr3_spmm(const rk_csr A, int6
   }
 }
 
+// ---------------------------------------------------------------------------
+// Scalar sliced-ELL (SELL-32, bdim == 1) for short uniform rows such as the
+// 7-point stencils of C2 and C5: a warp owns a slice of 32 rows, one row per
+// lane, and slot row t of the slice (32 values, 32 columns) is one 256-byte
+// and one 128-byte fully coalesced warp load. Each lane sums its row in CSR
+// order (padding slots hold 0 and a valid column), i.e. exactly scipy's
+// sequential csr_matvec order. 12 bytes per stored slot, no row pointers.
+// ---------------------------------------------------------------------------
+template <int U>
+__device__ __forceinline__ double sell1_row(const rk_csr& A, const double* __restrict__ x, int64_t slice, int lane) {
+  const int32_t base = __ldg(A.browptr + slice);
+  const int32_t width = (__ldg(A.browptr + slice + 1) - base) >> 5;
+  const int32_t* __restrict__ col = A.bcol + base + lane;
+  const double* __restrict__ val = A.bval + base + lane;
+  double s = 0.0;
+  for (int32_t t = 0; t < width; t += U) {  // U slot rows in flight per lane
+    int32_t c[U];
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool ok = t + u < width;
+      c[u] = ok ? ld_stream_s32(col + 32 * (t + u)) : 0;
+      v[u] = ok ? ld_stream_f64(val + 32 * (t + u)) : 0.0;
+    }
+    double xs[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) xs[u] = __ldg(x + c[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (t + u < width) s = fma(v[u], xs[u], s);
+  }
+  return s;
+}
+
+constexpr int kSell1U = 8;
+
+__global__ void __launch_bounds__(kSpmvThreads) k_sell1_spmv(const rk_csr A, const double* __restrict__ x,
+                                                            double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nsl = (A.n + 31) / 32;
+  const int64_t wpb = kSpmvThreads / 32;
+  for (int64_t sl = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); sl < nsl; sl += (int64_t)gridDim.x * wpb) {
+    const double s = sell1_row<kSell1U>(A, x, sl, lane);
+    const int64_t row = sl * 32 + lane;
+    if (row < A.n) y[row] = s;
+  }
+}
+
+__global__ void __launch_bounds__(kSpmvThreads) k_sell1_spmv_pcg(const rk_pcg_plan P) {
+  pdl_wait();
+  pdl_trigger();
+  if (P.st->done) return;
+  __shared__ double scratch[64];
+  const int64_t k = P.st->k;
+  const double* __restrict__ p = P.V + k * P.ldv;
+  double* __restrict__ Ap = P.AV + (P.ldav ? k * P.ldav : 0);
+  const int lane = threadIdx.x & 31;
+  const int64_t nsl = (P.n + 31) / 32;
+  const int64_t wpb = kSpmvThreads / 32;
+  double acc[2] = {0.0, 0.0};
+  for (int64_t sl = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); sl < nsl; sl += (int64_t)gridDim.x * wpb) {
+    const double s = sell1_row<kSell1U>(P.A, p, sl, lane);
+    const int64_t row = sl * 32 + lane;
+    if (row < P.n) {
+      Ap[row] = s;
+      const double pr = p[row];
+      acc[0] = fma(pr, s, acc[0]);
+      acc[1] = fma(pr, pr, acc[1]);
+    }
+  }
+  block_sum<2>(acc, scratch);
+  if (publish_and_check_last(acc, 2, P.partials, P.tickets + 0)) {
+    __shared__ double tot[2];
+    combine_partials(P.partials, gridDim.x, 2, tot);
+    if (threadIdx.x == 0) curvature_epilogue(P, tot[0], tot[1]);
+  }
+}
+
+// K2 on the scalar SELL view (blockIdx.y = column tile of CT columns): each
+// slot's value and column are loaded once for CT gathered columns; per column
+// the fma order is the SpMV's, so A X[:, j] is bitwise the SpMV of X[:, j].
+template <int CT>
+__global__ void __launch_bounds__(kSpmvThreads) k_sell1_spmm(const rk_csr A, int64_t m, const double* __restrict__ X,
+                                                            int64_t ldx, double* __restrict__ Y, int64_t ldy) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nsl = (A.n + 31) / 32;
+  const int64_t wpb = kSpmvThreads / 32;
+  const int64_t c0 = (int64_t)blockIdx.y * CT;
+  const int ncol = (int)(m - c0 < CT ? m - c0 : CT);
+  for (int64_t sl = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); sl < nsl; sl += (int64_t)gridDim.x * wpb) {
+    double acc[CT];
+#pragma unroll
+    for (int j = 0; j < CT; ++j) acc[j] = 0.0;
+    const int32_t base = __ldg(A.browptr + sl);
+    const int32_t width = (__ldg(A.browptr + sl + 1) - base) >> 5;
+    const int32_t* __restrict__ col = A.bcol + base + lane;
+    const double* __restrict__ val = A.bval + base + lane;
+    for (int32_t t = 0; t < width; t += kSell1U) {  // all slot loads of a pass before the gathers
+      int32_t c[kSell1U];
+      double v[kSell1U];
+#pragma unroll
+      for (int u = 0; u < kSell1U; ++u) {
+        const bool ok = t + u < width;
+        c[u] = ok ? ld_stream_s32(col + 32 * (t + u)) : 0;
+        v[u] = ok ? ld_stream_f64(val + 32 * (t + u)) : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < CT; ++j) {
+        if (j < ncol) {
+          const double* xc = X + (c0 + j) * ldx;
+          double xs[kSell1U];
+#pragma unroll
+          for (int u = 0; u < kSell1U; ++u) xs[u] = __ldg(xc + c[u]);
+#pragma unroll
+          for (int u = 0; u < kSell1U; ++u)
+            if (t + u < width) acc[j] = fma(v[u], xs[u], acc[j]);
+        }
+      }
+    }
+    const int64_t row = sl * 32 + lane;
+    if (row < A.n) {
+#pragma unroll
+      for (int j = 0; j < CT; ++j)
+        if (j < ncol) Y[(c0 + j) * ldy + row] = acc[j];
+    }
+  }
+}
+
 // Slot values from CSR values; perm < 0 marks padding (value 0).
 __global__ void k_bsr3_gather(int64_t total, const int32_t* __restrict__ perm, const double* __restrict__ val,
                               double* __restrict__ bval) {
@@ -636,6 +764,32 @@ static void launch_bsr3_spmv_pcg(const rk_pcg_plan& P, cudaStream_t s) {
   }
 }
 
+static int launch_sell1_spmv(const rk_csr& A, const double* x, double* y, cudaStream_t s) {
+  static const int cap = resident_blocks((const void*)rk::k_sell1_spmv, rk::kSpmvThreads);
+  const int64_t need = ((A.n + 31) / 32 + rk::kSpmvThreads / 32 - 1) / (rk::kSpmvThreads / 32);
+  rk::k_sell1_spmv<<<(int)std::max<int64_t>(1, std::min<int64_t>(cap, need)), rk::kSpmvThreads, 0, s>>>(A, x, y);
+  rkh::note_launch();
+  return cuda_check("rk_spmv (sell1)");
+}
+
+static void launch_sell1_spmv_pcg(const rk_pcg_plan& P, cudaStream_t s) {
+  // fixed blocks per SM (when resident) so the p'Ap / p'p partial order is fixed
+  static const int cap = std::min(resident_blocks((const void*)rk::k_sell1_spmv_pcg, rk::kSpmvThreads),
+                                  sm_count() * spmv_blocks_per_sm());
+  const int64_t need = ((P.n + 31) / 32 + rk::kSpmvThreads / 32 - 1) / (rk::kSpmvThreads / 32);
+  launch_pdl(rk::k_sell1_spmv_pcg, dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(cap, need))),
+             dim3(rk::kSpmvThreads), 0, s, P);
+}
+
+int launch_sell_gather(int64_t total, const int32_t* perm, const double* val, double* out, cudaStream_t s) {
+  if (total > 0) {
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 16));
+    rk::k_bsr3_gather<<<grid, 256, 0, s>>>(total, perm, val, out);
+    rkh::note_launch();
+  }
+  return cuda_check("rk_sell_gather");
+}
+
 int launch_bsr3_gather(int64_t nblk, const int32_t* perm, const double* val, double* bval, cudaStream_t s) {
   const int64_t total = 9 * nblk;
   if (total > 0) {
@@ -680,7 +834,7 @@ static void launch_spmv_l(const rk_csr& A, const double* x, double* y, cudaStrea
 }
 
 int launch_spmv(const rk_csr& A, const double* x, double* y, cudaStream_t s) {
-  if (A.bval) return launch_bsr3_spmv(A, x, y, s);
+  if (A.bval) return A.bdim == 1 ? launch_sell1_spmv(A, x, y, s) : launch_bsr3_spmv(A, x, y, s);
   switch (auto_lanes(A)) {
     case 1: launch_spmv_l<1>(A, x, y, s); break;
     case 2: launch_spmv_l<2>(A, x, y, s); break;
@@ -701,7 +855,10 @@ static void launch_spmv_pcg_l(const rk_pcg_plan& P, cudaStream_t s) {
 
 void launch_spmv_pcg(const rk_pcg_plan& P, cudaStream_t s) {
   if (P.A.bval) {
-    launch_bsr3_spmv_pcg(P, s);
+    if (P.A.bdim == 1)
+      launch_sell1_spmv_pcg(P, s);
+    else
+      launch_bsr3_spmv_pcg(P, s);
     return;
   }
   switch (auto_lanes(P.A)) {
@@ -759,7 +916,23 @@ static int spmm_bsr_ct() {
 int launch_spmm(const rk_csr& A, int64_t m, const double* X, int64_t ldx, double* Y, int64_t ldy,
                 cudaStream_t s) {
   if (m <= 0 || A.n <= 0) return 0;
-  if (A.bval) {
+  // The scalar SELL SpMM (k_sell1_spmm) measured 1.35-1.85 TB/s at C5 against
+  // 3.4 TB/s for the lanes-per-row CSR kernel, so it is opt-in (RK_SELL1_SPMM=1).
+  static const bool sell1_spmm = [] {
+    const char* e = getenv("RK_SELL1_SPMM");
+    return e && atoi(e) == 1;
+  }();
+  if (A.bval && A.bdim == 1 && sell1_spmm) {
+    constexpr int CT = 8;
+    static const int cap = resident_blocks((const void*)rk::k_sell1_spmm<CT>, rk::kSpmvThreads);
+    const int64_t tiles = (m + CT - 1) / CT;
+    const int64_t need = ((A.n + 31) / 32 + rk::kSpmvThreads / 32 - 1) / (rk::kSpmvThreads / 32);
+    const int64_t gx = std::max<int64_t>(1, std::min<int64_t>(need, std::max<int64_t>(1, cap / tiles)));
+    rk::k_sell1_spmm<CT><<<dim3((unsigned)gx, (unsigned)tiles), rk::kSpmvThreads, 0, s>>>(A, m, X, ldx, Y, ldy);
+    note_launch();
+    return cuda_check("rk_spmm (sell1)");
+  }
+  if (A.bval && A.bdim != 1) {
     switch (spmm_bsr_ct()) {
       case 2: launch_bsr3_spmm<2>(A, m, X, ldx, Y, ldy, s); break;
       case 8: launch_bsr3_spmm<8>(A, m, X, ldx, Y, ldy, s); break;

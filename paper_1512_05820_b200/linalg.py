@@ -213,6 +213,9 @@ def hstack_blocks(blocks, n: int, device, cap_extra: int = 0) -> torch.Tensor:
 _pattern_cache_lock = threading.Lock()
 _pattern_cache: list = []  # [(host rowptr, host col, _Pattern)]
 USE_BSR3 = os.environ.get("RK_BSR", "1") != "0"
+USE_SELL1 = os.environ.get("RK_SELL1", "1") != "0"
+SELL1_MAX_ROW = 16      # scalar SELL for short rows (7-point stencils); longer rows keep lanes-per-row CSR
+SELL1_MAX_PAD = 1.25    # ... and only when slices pad the pattern by at most 25%
 
 
 SELL_SLICE = 32  # block rows per slice (one warp, one block row per lane)
@@ -229,9 +232,50 @@ class _Bsr3:
         self.nreal = int(nreal)
 
 
+class _Sell1:
+    """Scalar sliced-ELL view (SELL-32, one row per lane): slice offsets (in
+    slots), the column of every slot and the permutation that gathers CSR
+    values into slot order (-1 = padding)."""
+
+    def __init__(self, sptr, scol, perm, nslot):
+        self.sptr, self.scol, self.perm, self.nslot = sptr, scol, perm, int(nslot)
+
+
 class _Pattern:
-    def __init__(self, rowptr: torch.Tensor, col: torch.Tensor, bsr: _Bsr3 | None):
-        self.rowptr, self.col, self.bsr = rowptr, col, bsr
+    def __init__(self, rowptr: torch.Tensor, col: torch.Tensor, bsr: _Bsr3 | None, sell: _Sell1 | None = None):
+        self.rowptr, self.col, self.bsr, self.sell = rowptr, col, bsr, sell
+
+
+def _sell1_from_host(rp: np.ndarray, ci: np.ndarray, n: int, device) -> _Sell1 | None:
+    """Scalar SELL-32 view of a pattern with short rows: slot (s, t, lane) =
+    sptr[s] + 32 t + lane holds entry t of row 32 s + lane; slices are padded
+    to their widest row with value 0 and the lane's own row as column."""
+    if n == 0 or ci.size == 0:
+        return None
+    rp = np.asarray(rp, dtype=np.int64)
+    lens = np.diff(rp)
+    if lens.max() > SELL1_MAX_ROW:
+        return None
+    nsl = (n + SELL_SLICE - 1) // SELL_SLICE
+    lp = np.zeros(nsl * SELL_SLICE, dtype=np.int64)
+    lp[:n] = lens
+    width = lp.reshape(nsl, SELL_SLICE).max(axis=1)
+    sptr = np.zeros(nsl + 1, dtype=np.int64)
+    np.cumsum(width * SELL_SLICE, out=sptr[1:])
+    nslot = int(sptr[-1])
+    if nslot > SELL1_MAX_PAD * ci.size or nslot >= 2**31:
+        return None
+    row = np.repeat(np.arange(n, dtype=np.int64), lens)
+    t_loc = np.arange(ci.size, dtype=np.int64) - rp[row]
+    slot = sptr[row // SELL_SLICE] + t_loc * SELL_SLICE + row % SELL_SLICE
+    sl_of = np.repeat(np.arange(nsl, dtype=np.int64), width * SELL_SLICE)
+    pos = np.arange(nslot, dtype=np.int64) - sptr[sl_of]
+    scol = np.minimum(sl_of * SELL_SLICE + pos % SELL_SLICE, n - 1)
+    scol[slot] = np.asarray(ci, dtype=np.int64)
+    perm = np.full(nslot, -1, dtype=np.int64)
+    perm[slot] = np.arange(ci.size, dtype=np.int64)
+    to = lambda arr: torch.from_numpy(np.ascontiguousarray(arr, dtype=np.int32)).to(device)  # noqa: E731
+    return _Sell1(to(sptr), to(scol), to(perm), nslot)
 
 
 def _bsr3_from_host(rp: np.ndarray, ci: np.ndarray, n: int, device) -> _Bsr3 | None:
@@ -303,7 +347,8 @@ def _device_pattern(rowptr: np.ndarray, col: np.ndarray, device, n: int) -> _Pat
     dr = torch.from_numpy(np.ascontiguousarray(rowptr, dtype=np.int32)).to(device)
     dc = torch.from_numpy(np.ascontiguousarray(col, dtype=np.int32)).to(device)
     bsr = _bsr3_from_host(rowptr, col, n, device) if USE_BSR3 else None
-    p = _Pattern(dr, dc, bsr)
+    sell = _sell1_from_host(rowptr, col, n, device) if (USE_SELL1 and bsr is None) else None
+    p = _Pattern(dr, dc, bsr, sell)
     with _pattern_cache_lock:
         _pattern_cache.insert(0, (rowptr, col, p))
         del _pattern_cache[2:]
@@ -373,6 +418,17 @@ class SparseSpdMatrix:
             c = self._csr
             c.nblk, c.browptr, c.bcol, c.bval = bsr.nblk, bsr.browptr.data_ptr(), bsr.bcol.data_ptr(), \
                 self.bval.data_ptr()
+            c.bdim = 3
+        sell = getattr(pattern, "sell", None)
+        if self.bval is None and sell is not None and self.lanes == 0:
+            # scalar SELL-32 values for the SpMV / SpMM kernels (one gather per matrix)
+            self.bval = torch.empty(sell.nslot, dtype=F64, device=self.device)
+            nat.check(nat.lib().rk_sell_gather(sell.nslot, sell.perm.data_ptr(), vals.data_ptr(),
+                                               self.bval.data_ptr(), nat.stream_ptr(self.device)), "sell gather")
+            c = self._csr
+            c.nblk, c.browptr, c.bcol, c.bval = sell.nslot, sell.sptr.data_ptr(), sell.scol.data_ptr(), \
+                self.bval.data_ptr()
+            c.bdim = 1
         self._diag = None
         self._dinv = None
         self._bad_diag = None

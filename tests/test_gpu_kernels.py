@@ -304,3 +304,28 @@ def test_c5_small_blocked_gram_matches_reference(pk):
     for j in range(20):
         s = np.sign(got[:, j] @ ref[:, j])
         assert np.linalg.norm(s * got[:, j] - ref[:, j]) <= 1e-8 * np.linalg.norm(ref[:, j])
+
+
+def test_scalar_sell_spmv_and_spmm(pk):
+    """7-point stencil (C2/C5 shape, reduced): the scalar SELL-32 view is chosen,
+    SpMV matches scipy to rounding, SpMM (lanes-per-row CSR kernel unless
+    RK_SELL1_SPMM=1) agrees with it, and a forced lanes-per-row CSR agrees."""
+    import scipy.sparse
+
+    from paper_1512_05820_b200.linalg import as_block, spmm
+    from paper_1512_05820_b200.problems import laplacian3d
+
+    L = laplacian3d(24, 20, 36)
+    A = pk.SparseSpdMatrix(L.n, L.row_offsets, L.col_indices, L.values)
+    assert A.csr.bdim == 1 and A.bval is not None
+    rng = np.random.default_rng(7)
+    X = rng.standard_normal((L.n, 11))
+    ref = scipy.sparse.csr_matrix((L.values, L.col_indices, L.row_offsets), shape=(L.n, L.n)) @ X
+    Y = spmm(A, as_block(X)).cpu().numpy()
+    for j in range(11):
+        y = pk.spmv(A, X[:, j]).cpu().numpy()
+        np.testing.assert_allclose(Y[:, j], y, rtol=1e-14, atol=1e-14 * np.abs(y).max())
+        np.testing.assert_allclose(y, ref[:, j], rtol=1e-14, atol=1e-14 * np.abs(ref[:, j]).max())
+    B = pk.SparseSpdMatrix(L.n, L.row_offsets, L.col_indices, L.values, lanes=2)
+    assert B.csr.bdim == 0 and B.bval is None
+    np.testing.assert_allclose(pk.spmv(B, X[:, 0]).cpu().numpy(), Y[:, 0], rtol=1e-14, atol=1e-13)
