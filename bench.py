@@ -56,13 +56,15 @@ def parse():
     ap.add_argument("--grid", type=int, default=64)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--workload", default="c3", choices=["c3", "c2", "c5"],
+    ap.add_argument("--workload", default="c3", choices=["c3", "c2", "c4", "c5"],
                     help="c3 (default, the north-star sequence), c2 (128^3 diffusion sequence), "
-                         "c5 (POD truncation microbench)")
+                         "c4 (128x128x64 dynamic elasticity, snapshot to ~3000), c5 (POD truncation microbench)")
     ap.add_argument("--m", type=int, default=2048, help="c5: snapshot columns")
     args = ap.parse_args()
     if args.workload == "c2" and args.systems == 40:
         args.systems = 30
+    if args.workload == "c4" and args.systems == 40:
+        args.systems = 60
     return args
 
 
@@ -72,6 +74,11 @@ WORKLOADS = {
            "l2": "inputs larger than L2 (552 MB of 3x3-block matrix streamed per SpMV, 20 GB of matrices); no flush"},
     "c2": {"rtol": 1e-4, "cap": 40, "data": "synthetic (seeded C2 generator, BASELINE configs[1] shapes)",
            "l2": "inputs larger than L2 (175 MB of CSR streamed per SpMV, 3.5 GB of matrices); no flush"},
+    # C4: the snapshot accumulates Krylov vectors up to the storage cap (SURVEY 8d flags cap ~ 3000 as a
+    # builder's choice); every accumulated column is a stage-1 column (nu_w = 1), max_dim 60 after truncation
+    "c4": {"rtol": 1e-6, "cap": 3000, "max_dim": 60,
+           "data": "synthetic (seeded C4 generator: K + M/dt^2, dt = 0.05, seeded load history; BASELINE configs[3])",
+           "l2": "inputs larger than L2 (2.2 GB of 3x3-block matrix streamed per SpMV); no flush"},
 }
 
 
@@ -81,14 +88,16 @@ def make_sequence(args, seed_offset=0, p=None):
     p = args.systems if p is None else p
     if args.workload == "c2":
         return diffusion3d_sequence(128, p=p, rtol=1e-4, seed=2 + seed_offset)
+    if args.workload == "c4":
+        return elasticity_sequence((128, 128, 64), p=p, rtol=1e-6, seed=4 + seed_offset, dynamic=True, dt=0.05)
     return elasticity_sequence((args.grid,) * 3, p=p, rtol=1e-5, seed=3 + seed_offset)
 
 
 def workload_config(args, n=None, nnz=None):
     w = WORKLOADS[args.workload]
-    name = (f"C2 variable-coefficient diffusion 128^3, {args.systems}-system recycled sequence"
-            if args.workload == "c2" else
-            f"C3 Q1 elasticity {args.grid}^3 elements, {args.systems}-system recycled sequence")
+    name = {"c2": f"C2 variable-coefficient diffusion 128^3, {args.systems}-system recycled sequence",
+            "c4": f"C4 Q1 elasticity 128x128x64 elements, K + M/dt^2, {args.systems}-system recycled sequence",
+            }.get(args.workload, f"C3 Q1 elasticity {args.grid}^3 elements, {args.systems}-system recycled sequence")
     return {
         "workload": name,
         "systems": args.systems,
@@ -97,15 +106,16 @@ def workload_config(args, n=None, nnz=None):
         "mode": args.mode,
         "preconditioner": "jacobi",
         "rtol": w["rtol"],
-        "truncation": f"pod-a-rbf nu_y=1 nu_w=1 storage_cap={w['cap']} max_dim={w['cap']}",
+        "truncation": f"pod-a-rbf nu_y=1 nu_w=1 storage_cap={w['cap']} max_dim={w.get('max_dim', w['cap'])}",
         "l2": w["l2"],
         "parallelism": "replicas (one independent sequence per GPU)",
     }
 
 
 def solver_config(pk, args):
-    cap = WORKLOADS[args.workload]["cap"]
-    tr = pk.TruncationConfig(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=cap, max_dim=cap)
+    w = WORKLOADS[args.workload]
+    tr = pk.TruncationConfig(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=w["cap"],
+                             max_dim=w.get("max_dim", w["cap"]))
     return pk.SolverConfig(truncation=tr, mode=args.mode)
 
 
@@ -231,8 +241,11 @@ def run_b200(args, rank, world, dist):
     nnz = host_specs[0].A.nnz
     # device-resident inputs for `value`
     dev_specs = []
+    uploaded = {}  # invariant-matrix sequences (C4) share one device matrix
     for s in host_specs:
-        A = pk.SparseSpdMatrix.from_host(s.A)
+        if id(s.A) not in uploaded:
+            uploaded[id(s.A)] = pk.SparseSpdMatrix.from_host(s.A)
+        A = uploaded[id(s.A)]
         dev_specs.append(pk.LinearSystemSpec(A=A, b=torch.from_numpy(s.b).to(dev), xbar=None, tol=s.tol))
     dseq = pk.SystemSequence(n, dev_specs, C=seq.C)
     cfg = solver_config(pk, args)
@@ -270,25 +283,6 @@ def run_b200(args, rank, world, dist):
     # q = c'x of the last timed sequence (D2H only after timing)
     q_last = float(seq.C[0] @ xs[-1].cpu().numpy())
 
-    # e2e: the public API from host CSR arrays; H2D of values+rhs and D2H of x inside
-    e2e = None
-    if not args.no_e2e:
-        hseq = pk.SystemSequence(n, host_specs, C=seq.C)
-        h2d = sum(s.A.values.nbytes + s.b.nbytes for s in host_specs)
-        d2h = n * 8 * len(host_specs)
-        barrier(dist)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        xs_e, reps_e, _ = pk.run_sequence(hseq, cfg, precond_factory=jac)
-        xh = [x.cpu().numpy() for x in xs_e]
-        torch.cuda.synchronize()
-        t_e2e = max_over_ranks(time.perf_counter() - t0, dist)
-        e2e = {"value": round(t_e2e / world, 4), "unit": UNIT, "h2d_bytes_per_step": int(h2d * world),
-               "d2h_bytes_per_step": int(d2h * world),
-               "solve_wall_sum_s": round(sum(r.wall_time for r in reps_e), 3),
-               "path": "run_sequence over host CSR (reference-style SparseSpdMatrix fields), solutions copied back"}
-        del xh
-
     avg = [ms[i] / max(cnt[i], 1) for i in range(4)]
     peaks = _peaks()
     A0 = dev_specs[0].A
@@ -305,6 +299,32 @@ def run_b200(args, rank, world, dist):
     else:
         fmt = "CSR (fp64 values, int32 columns)"
         alg_bytes = spmv_bytes(n, nnz)
+    dev = A0.device
+    # e2e: the public API from host CSR arrays; H2D of values+rhs and D2H of x inside
+    e2e = None
+    if not args.no_e2e and args.workload == "c4":
+        # C4 fills HBM (two ~80 GB snapshot blocks): drop the device-resident
+        # inputs of the `value` leg before the host-input run
+        del dev_specs, dseq, xs, A0, A
+        uploaded.clear()
+        torch.cuda.empty_cache()
+    if not args.no_e2e:
+        hseq = pk.SystemSequence(n, host_specs, C=seq.C)
+        h2d = sum(s.b.nbytes for s in host_specs) + sum({id(s.A): s.A.values.nbytes for s in host_specs}.values())
+        d2h = n * 8 * len(host_specs)
+        barrier(dist)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        xs_e, reps_e, _ = pk.run_sequence(hseq, cfg, precond_factory=jac)
+        xh = [x.cpu().numpy() for x in xs_e]
+        torch.cuda.synchronize()
+        t_e2e = max_over_ranks(time.perf_counter() - t0, dist)
+        e2e = {"value": round(t_e2e / world, 4), "unit": UNIT, "h2d_bytes_per_step": int(h2d * world),
+               "d2h_bytes_per_step": int(d2h * world),
+               "solve_wall_sum_s": round(sum(r.wall_time for r in reps_e), 3),
+               "path": "run_sequence over host CSR (reference-style SparseSpdMatrix fields), solutions copied back"}
+        del xh
+
     ach = alg_bytes / (avg[0] * 1e-3) / 1e9
     traffic = None
     if args.workload == "c3":  # the committed ncu capture is of the C3 SELL kernel
@@ -313,7 +333,7 @@ def run_b200(args, rank, world, dist):
                 traffic = json.load(fh).get("k_spmv_pcg", {}).get("dram_bytes_per_launch")
         except Exception:
             pass
-    gram = _gram_roofline(dev_specs[0].A, reports)
+    gram = _gram_roofline(n, dev, reports)
     iters = [r.stage3_iters for r in reports]
     sched = {"stage3_iters": iters, "truncated": [bool(r.truncated) for r in reports],
              "basis_dim": [r.basis_dim for r in reports], "grown": [r.basis_dim + r.stage3_iters for r in reports]}
@@ -368,7 +388,7 @@ def run_b200(args, rank, world, dist):
 DMMA_PEAK_TFLOPS = 37.1  # B200 FP64 tensor (DMMA) peak measured by scripts/dmma_probe.cu (profiles/dmma_peak_r01.json)
 
 
-def _gram_roofline(A, reports):
+def _gram_roofline(n, dev, reports):
     """BASELINE's second metric: the truncation Gram Z'AZ (rk_gram_upper from
     cached products, DMMA) at the sequence's own truncation width, timed with
     CUDA events after the timed region (3 launches, random data of that shape),
@@ -383,8 +403,9 @@ def _gram_roofline(A, reports):
         return None
     m = int(np.median(grown))
     y_old = min(60, m - 1)
-    n = A.n
-    dev = A.device
+    if 2 * n * m * 8 > 40e9:  # C4: the sequence's own buffers already hold most of HBM
+        return {"kernel": "K7 k_gram (rk_gram_upper)", "n": n, "m": m,
+                "skipped": "shape probe needs 2 N x m blocks (> 40 GB); see scripts/gram_probe.py"}
     g = torch.Generator(device=dev).manual_seed(1)
     Z, AY, AV = empty_block(n, m, dev), empty_block(n, y_old, dev), empty_block(n, m - y_old, dev)
     for t in (Z, AY, AV):
@@ -677,12 +698,14 @@ def cpu_sample(host_specs, sched, cap=60, label="C3", budget_s=20.0):
             pass
         return (time.perf_counter() - t0) / k
 
-    k0 = 12
+    k0 = 12 if A.nnz < 10**8 else 6
     t_it0 = iters_cost(None, k0)
-    Y = np.linalg.qr(rng.standard_normal((n, cap)))[0]
-    t_it60 = iters_cost(Y, 8)
-    # truncation sample: SpMM + Gram with 32 columns, eigh at full width, S @ coef sample
-    s_cols = 32
+    ms = min(cap, 60)  # projected sample width; per-column cost scales the other widths
+    Y = np.linalg.qr(rng.standard_normal((n, ms)))[0]
+    t_itm = iters_cost(Y, 8 if A.nnz < 10**8 else 4)
+    t_col = max(t_itm - t_it0, 0.0) / ms
+    # truncation sample: SpMM + Gram with s_cols columns, eigh at full width, S @ coef sample
+    s_cols = 32 if A.nnz < 10**8 else 8
     Z = rng.standard_normal((n, s_cols))
     t0 = time.perf_counter()
     AZ = A @ Z
@@ -702,10 +725,11 @@ def cpu_sample(host_specs, sched, cap=60, label="C3", budget_s=20.0):
 
     total = 0.0
     if sched:
-        for j, (k, g) in enumerate(zip(sched["stage3_iters"], sched["grown"])):
-            total += k * (t_it0 if j == 0 else t_it60)
-            if j > 0:
-                total += cap * t_spmm + cap * cap * t_gram_unit   # stage-1 assemble_gram of W
+        widths = sched.get("basis_dim") or [0] + [cap] * (len(sched["stage3_iters"]) - 1)
+        for k, g, w in zip(sched["stage3_iters"], sched["grown"], widths):
+            total += k * (t_it0 + w * t_col)                      # stage-3 iterations projected against w
+            if w:
+                total += w * t_spmm + w * w * t_gram_unit        # stage-1 assemble_gram of W
             if g > cap:  # truncation: SpMM + Gram of the grown block, eigh, reconstruction
                 total += g * t_spmm + g * g * t_gram_unit + t_evd * (g / grown) ** 3 + g * t_rec_unit
     return {
@@ -713,12 +737,12 @@ def cpu_sample(host_specs, sched, cap=60, label="C3", budget_s=20.0):
         "unit": UNIT,
         "cores": cores,
         "kind": "port",
-        "sample": (f"oracle on {label} system 1: {k0} plain PCG iterations ({t_it0*1e3:.0f} ms/it), 8 iterations "
-                   f"projected against {cap} columns ({t_it60*1e3:.0f} ms/it), a {s_cols}-column SpMM+Gram, "
+        "sample": (f"oracle on {label} system 1: {k0} plain PCG iterations ({t_it0*1e3:.0f} ms/it), iterations "
+                   f"projected against {ms} columns ({t_itm*1e3:.0f} ms/it), a {s_cols}-column SpMM+Gram, "
                    f"S@coef and eigh({grown}); scaled to the sequence with the GPU run's schedule "
                    f"({sum(sched['stage3_iters']) if sched else 0} stage-3 iterations, extrapolated)"),
-        "components_s": {"t_iter_plain": t_it0, "t_iter_m60": t_it60, "t_spmm_per_col": t_spmm,
-                         "t_gram_per_col2": t_gram_unit, "t_evd_full": t_evd},
+        "components_s": {"t_iter_plain": t_it0, "t_iter_projected": t_itm, "t_per_projected_column": t_col,
+                         "t_spmm_per_col": t_spmm, "t_gram_per_col2": t_gram_unit, "t_evd_full": t_evd},
     }
 
 

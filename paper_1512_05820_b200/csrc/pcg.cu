@@ -56,7 +56,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 constexpr int kUpdThreads = 256;
 constexpr int kProjChunk = 1024;                 // rows per update block
 constexpr int kProjCols = 32;                    // cross columns per update block (4 per warp)
-constexpr int kMaxProj = 2048;                   // projection width of the fused path
+constexpr int kMaxProj = 4096;                   // projection width of the fused path (C4: ~3000)
 constexpr int kStageFactor = 96;                 // Linv staged in shared memory up to this width
 #ifndef RK_DIR_UNROLL
 #define RK_DIR_UNROLL 12
@@ -66,6 +66,7 @@ constexpr int kStageFactor = 96;                 // Linv staged in shared memory
 #endif
 constexpr int kDirUnroll = RK_DIR_UNROLL;          // B loads in flight per row in the direction kernel
 constexpr int kDirMinBlocks = RK_DIR_MINB;
+constexpr int kWideSolve = 256;                  // dense factors wider than this: mu on the whole GPU
 constexpr int kFuseMax = 64;                     // widths whose finish runs in the update kernel's tail
 constexpr int kMaxGroups = 256;                  // chunk groups of the fused two-level combine
 
@@ -426,7 +427,7 @@ __global__ void __launch_bounds__(kUpdThreads, 4) k_pcg_update(const rk_pcg_plan
 // block reduction (deterministic, one L2 round trip instead of a serial walk).
 // Linv does not change during a run, so narrow factors are staged in shared
 // memory before waiting on the update kernel (overlapping its tail).
-__global__ void __launch_bounds__(256) k_pcg_finish(const rk_pcg_plan P, int entry, int64_t nchunks) {
+__global__ void __launch_bounds__(256) k_pcg_finish(const rk_pcg_plan P, int entry, int64_t nchunks, int wide) {
   rk_pcg_state* st = P.st;
   extern __shared__ double dyn[];      // Ls[w*w] (staged) | red[2 + m] | ysm[2 w]
   __shared__ double scratch[32];
@@ -458,8 +459,47 @@ __global__ void __launch_bounds__(256) k_pcg_finish(const rk_pcg_plan P, int ent
   __threadfence();
   for (int64_t j = threadIdx.x; j < nv; j += blockDim.x) red[j] = __ldcg(sums + j);
   __syncthreads();
-  if (pcg_scalars(P, entry, red) || m == 0) return;
+  if (pcg_scalars(P, entry, red) || m == 0 || wide) return;  // wide: k_pcg_musolve follows
   solve_factor(P, red + 2, red + nv, staged ? Ls : nullptr, P.mu);
+}
+
+// mu = F^{-1} c for wide dense factors (w > kWideSolve, F^{-1} held full and
+// symmetric): a warp per row, lanes over the row's entries (coalesced, since
+// row i of the symmetric F^{-1} is its column i), butterfly sum; trailing
+// sqrt-diagonal entries are a division. Spread over the whole GPU instead of
+// the finish kernel's last block (C4, w ~ 3000: 72 MB of F^{-1} per iteration
+// read by one SM took 1.3 ms). c = the combined cross' z sums of k_pcg_finish.
+__global__ void __launch_bounds__(256) k_pcg_musolve(const rk_pcg_plan P, int64_t nchunks) {
+  rk_pcg_state* st = P.st;
+  pdl_wait();
+  pdl_trigger();
+  if (st->done) return;
+  const int64_t m = P.m, w = P.wchol;
+  const double* __restrict__ c = P.partials + (2 + m) * nchunks + 2;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < m; i += warps) {
+    if (i < w) {
+      const double* __restrict__ row = P.L + i * P.ldl;
+      double s = 0.0;
+      int64_t j = lane;
+      for (; j + 96 < w; j += 128) {  // 4 loads in flight per lane
+        const double a0 = __ldg(row + j), a1 = __ldg(row + j + 32), a2 = __ldg(row + j + 64), a3 = __ldg(row + j + 96);
+        const double c0 = __ldcg(c + j), c1 = __ldcg(c + j + 32), c2 = __ldcg(c + j + 64), c3 = __ldcg(c + j + 96);
+        s = fma(a0, c0, s);
+        s = fma(a1, c1, s);
+        s = fma(a2, c2, s);
+        s = fma(a3, c3, s);
+      }
+      for (; j < w; j += 32) s = fma(__ldg(row + j), __ldcg(c + j), s);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) P.mu[i] = s;
+    } else if (lane == 0) {
+      const double d = P.sqd[i - w];
+      P.mu[i] = __ldcg(c + i) / (d * d);
+    }
+  }
 }
 
 // K5: new direction into V[:, k+1] (entry: V[:, 0]).
@@ -583,7 +623,12 @@ static void launch_update(const rk_pcg_plan& P, int entry, cudaStream_t s, bool 
   if (mark) prof_mark(2, s);
   if (fused) return;
   const unsigned fgrid = (unsigned)std::min<int64_t>(2 + P.m, 4096);
-  launch_pdl(rk::k_pcg_finish, dim3(fgrid), dim3(256), finish_smem(P.m, P.wchol), s, P, entry, nch);
+  const int wide = (P.linv_full && P.wchol > rk::kWideSolve) ? 1 : 0;
+  launch_pdl(rk::k_pcg_finish, dim3(fgrid), dim3(256), finish_smem(P.m, wide ? 0 : P.wchol), s, P, entry, nch, wide);
+  if (wide) {
+    const unsigned mgrid = (unsigned)std::min<int64_t>((P.m + 7) / 8, (int64_t)sm_count() * 8);
+    launch_pdl(rk::k_pcg_musolve, dim3(mgrid), dim3(256), 0, s, P, nch);
+  }
 }
 
 static void launch_direction(const rk_pcg_plan& P, int entry, int64_t kmax, cudaStream_t s) {

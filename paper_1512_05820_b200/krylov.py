@@ -725,19 +725,44 @@ class DirectSolveResult:
     what: np.ndarray
     rhat: DenseLowerTriangular
     aw: torch.Tensor  # cached A @ W on the device
+    gram: np.ndarray | None = None  # W'AW as factored (host), for callers that extend it
 
 
-def direct_reduced_solve(A, b, W, sink: InstrumentationSink | None = None) -> DirectSolveResult:
+def direct_reduced_solve(A, b, W, sink: InstrumentationSink | None = None, *,
+                         aw_out=None, known=None) -> DirectSolveResult:
     """Galerkin solve over range(W) by Cholesky of W'AW (krylov.py:396-411):
     SpMM + DMMA Gram on the device, dpotrf and the two triangular solves on
-    the host (w x w)."""
-    from .linalg import assemble_gram
+    the host (w x w). ``aw_out`` (N x w device block) receives A W.
+
+    ``known = (w0, G0)``: the caller guarantees that ``aw_out[:, :w0]`` already
+    holds A W[:, :w0] for this very matrix and G0 = W[:, :w0]' A W[:, :w0]
+    (an invariant matrix with a snapshot grown in place, C1/C4). Only the new
+    columns are multiplied and contracted -- A W[:, :w0] would come out of the
+    SpMM bit for bit the same -- and the sink is charged exactly as the full
+    assemble_gram (one gram, w matvecs)."""
+    from .linalg import assemble_gram, gram as gram_xty, spmm
 
     A = as_matrix(A)
     Wd = as_block(W, A.device)
     bd = as_vector(b, A.device)
-    G, AW = assemble_gram(A, Wd, sink)
-    g = to_numpy(G)
-    rhat = dense_cholesky(0.5 * (g + g.T))
+    w = int(Wd.shape[1])
+    if known is not None and aw_out is not None and 0 < known[0] <= w:
+        w0, G0 = known
+        if sink is not None:
+            sink.add_gram()
+            sink.add_matvec(w)
+        AW = aw_out
+        g = np.empty((w, w))
+        g[:w0, :w0] = G0
+        if w > w0:
+            spmm(A, Wd[:, w0:], out=AW[:, w0:])
+            gn = to_numpy(gram_xty(Wd, AW[:, w0:]))       # W' A W_new, w x (w - w0)
+            g[:, w0:] = gn
+            g[w0:, :w0] = gn[:w0].T
+    else:
+        G, AW = assemble_gram(A, Wd, sink, out=aw_out)
+        g = to_numpy(G)
+    g = 0.5 * (g + g.T)
+    rhat = dense_cholesky(g)
     what = rhat.solve_spd(to_numpy(gemv_t(Wd, bd)))
-    return DirectSolveResult(what=what, rhat=rhat, aw=AW)
+    return DirectSolveResult(what=what, rhat=rhat, aw=AW, gram=g)

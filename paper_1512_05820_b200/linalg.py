@@ -79,6 +79,27 @@ def empty_block(n: int, m: int, device, cap: int | None = None) -> torch.Tensor:
     return store[: int(m), : int(n)].t()
 
 
+def block_capacity(B: torch.Tensor) -> int:
+    """Columns the storage behind a block view can hold starting at its first
+    column (0 when it is not a column-0 view of an empty_block store)."""
+    base = B._base if B._base is not None else None
+    if base is None or base.dim() != 2 or B.dim() != 2 or B.storage_offset() != base.storage_offset():
+        return 0
+    if int(B.shape[1]) > 1 and int(B.stride(1)) != int(base.shape[1]):
+        return 0
+    if int(B.shape[0]) > int(base.shape[1]):
+        return 0
+    return int(base.shape[0])
+
+
+def grow_block(B: torch.Tensor, m: int) -> torch.Tensor | None:
+    """View of the first ``m`` columns of B's storage (B's columns unchanged,
+    columns beyond them uninitialised), or None when the capacity is short."""
+    if block_capacity(B) < m:
+        return None
+    return B._base[: int(m), : int(B.shape[0])].t()
+
+
 def zeros_block(n: int, m: int, device, cap: int | None = None) -> torch.Tensor:
     b = empty_block(n, m, device, cap)
     if m:
@@ -761,9 +782,10 @@ def weighted_inner(A: SparseSpdMatrix, x, y) -> float:
     return float(dot(xd, Ay).cpu())
 
 
-def assemble_gram(A: SparseSpdMatrix, B, sink: InstrumentationSink | None = None):
+def assemble_gram(A: SparseSpdMatrix, B, sink: InstrumentationSink | None = None, out: torch.Tensor | None = None):
     """(B'AB, AB) (linalg.py:160-174): SpMM then the DMMA Gram; counts one gram
-    assembly plus one matvec per column, exactly like the reference."""
+    assembly plus one matvec per column, exactly like the reference. ``out``
+    (N x m device block) receives AB instead of a fresh allocation."""
     A = as_matrix(A)
     Bd = as_block(B, A.device)
     if Bd.shape[0] != A.n:
@@ -771,7 +793,7 @@ def assemble_gram(A: SparseSpdMatrix, B, sink: InstrumentationSink | None = None
     if sink is not None:
         sink.add_gram()
         sink.add_matvec(int(Bd.shape[1]))
-    AB = spmm(A, Bd)
+    AB = spmm(A, Bd, out=out)
     return gram(Bd, AB), AB
 
 

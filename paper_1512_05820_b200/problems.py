@@ -366,7 +366,8 @@ class ElasticityAssembler:
         return np.concatenate([self.slots[(d0, c, c)][None, :] for c in range(3)]).T.reshape(-1)
 
     def face_load(self, traction) -> np.ndarray:
-        """Consistent-area nodal forces of a uniform traction on the x = 1 face."""
+        """Consistent-area nodal forces of a traction on the x = 1 face: a
+        uniform 3-vector, or a nodal field of shape (nez + 1, ney + 1, 3)."""
         nex, ney, nez = self.ne
         fz, fy, fx = self.fshape
         wy = np.full(fy, self.h)
@@ -407,15 +408,22 @@ def elasticity_sequence(ne=(64, 64, 64), p: int = 40, rtol: float = 1e-5, seed: 
         vals = vals_E.copy()
         vals[asm.diagonal_slots()] += asm.lumped_mass_diagonal() / dt ** 2
         A = HostCsr(N, rowptr, col, vals)
-        modes = rng.standard_normal((4, 3))
-        freqs = 0.5 + rng.random(4)
-        phases = 2 * math.pi * rng.random(4)
+        fz, fy, _ = asm.fshape
+        # seeded load history: a smooth random traction field on the x = 1 face
+        # that drifts by a fresh smooth random increment every step (each system
+        # brings one new load direction) plus a slowly rotating uniform part
+        load_seed = int(rng.integers(2**31))
+        base = rng.standard_normal(3)
 
         def gen():
+            r = np.random.default_rng(load_seed)
+            trac = np.zeros((fz, fy, 3))
             for i in range(1, p + 1):
                 t = i * dt
-                trac = sum(modes[q] * math.sin(freqs[q] * 2 * math.pi * t + phases[q]) for q in range(4))
-                b = asm.face_load(trac)
+                inc = np.stack([gaussian_field((fz, fy), 4.0, r) for _ in range(3)], axis=-1)
+                trac = trac + 0.5 * inc
+                th = 2 * math.pi * 0.5 * t
+                b = asm.face_load(trac + base * math.cos(th))
                 yield LinearSystemSpec(A=A, b=b, xbar=None, tol=rtol * float(np.linalg.norm(b)))
 
     return SystemSequence(N, gen, C=c[None, :], p_hint=p, metadata=meta)

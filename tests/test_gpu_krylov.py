@@ -154,3 +154,29 @@ def test_batching_does_not_change_results(pk):
     b = pk.augmented_pcg(A, d["b"], d["yhat0"], d["Y"], tol=1e-10, mode="fom", max_iter=400, batch=64)
     assert a.k == b.k
     assert np.array_equal(_np(a.x), _np(b.x))  # deterministic reductions: bitwise
+
+
+def test_wide_projection_matches_oracle(pk):
+    """Projection width 300 (> the 256 above which mu = F^{-1} c is spread over
+    the whole GPU by k_pcg_musolve instead of the finish kernel's last block):
+    same iteration count and solution as the oracle on C1's Poisson matrix."""
+    from oracle import recycle_oracle as O
+    from paper_1512_05820_b200.problems import poisson2d_matrix
+
+    L = poisson2d_matrix(64)
+    A = pk.SparseSpdMatrix(L.n, L.row_offsets, L.col_indices, L.values)
+    As = O.as_csr(L)
+    rng = np.random.default_rng(11)
+    Y = np.linalg.qr(rng.standard_normal((L.n, 300)))[0]
+    b = rng.standard_normal(L.n)
+    yhat0 = np.linalg.solve(Y.T @ (As @ Y), Y.T @ b)
+    M = pk.build_preconditioner("jacobi", A)
+    tol = 1e-8 * np.linalg.norm(b)
+    res = pk.augmented_pcg(A, b, yhat0, Y, precond=M, tol=tol, mode="cg", max_iter=2000)
+    t = O.Tally()
+    proj = O.assembled_projection(lambda v: O.matvec(As, v, t), Y)
+    ref = O.aug_pcg(lambda v: O.matvec(As, v, t), b, yhat0, Y, proj, 1.0 / As.diagonal(), tol, mode="cg",
+                    max_iter=2000, tally=t)
+    assert abs(res.k - ref.k) <= 2
+    x = _np(res.x)
+    assert np.linalg.norm(x - ref.x) <= 1e-8 * np.linalg.norm(ref.x)

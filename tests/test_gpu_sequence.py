@@ -210,3 +210,29 @@ def test_not_converged_stage3_continues_and_stops(pk):
     assert len(reps) == 1 and not reps[0].converged and reps[0].stage3_iters == 5
     xs, reps, _ = pk.run_sequence(gio.sequence(d), cfg, precond_factory=jac, stop_on_failure=False)
     assert len(reps) == int(d["p"]) and not any(r.converged for r in reps)
+
+
+def test_invariant_matrix_stage1_reuses_products(pk):
+    """Invariant matrix, snapshot accumulating without truncation (C4 pattern):
+    with one shared device matrix object stage 1 multiplies only the new
+    columns of W (the cached A W columns are what the SpMM would give bit for
+    bit); the run matches one with a fresh matrix object per system (full
+    stage-1 SpMM + Gram every time) with identical counters."""
+    from paper_1512_05820_b200.problems import poisson2d_sequence
+
+    seq = poisson2d_sequence(32, p=6)
+    specs = list(seq)
+    A0 = pk.SparseSpdMatrix.from_host(specs[0].A)
+    shared = pk.SystemSequence(seq.n, [pk.LinearSystemSpec(A=A0, b=s.b, xbar=None, tol=s.tol) for s in specs],
+                               C=seq.C)
+    fresh = pk.SystemSequence(seq.n, [pk.LinearSystemSpec(A=A0.with_values(A0.values.clone()), b=s.b, xbar=None,
+                                                          tol=s.tol) for s in specs], C=seq.C)
+    tr = dict(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=1000, max_dim=60)
+    xs_a, rep_a, _ = _run(pk, shared, tr, "cg", "jacobi")
+    xs_b, rep_b, _ = _run(pk, fresh, tr, "cg", "jacobi")
+    assert rep_a[-1].basis_dim > 0 and not any(r.truncated for r in rep_a)
+    assert [r.matvecs for r in rep_a] == [r.matvecs for r in rep_b]
+    assert [r.stage3_iters for r in rep_a] == [r.stage3_iters for r in rep_b]
+    for a, b in zip(xs_a, xs_b):
+        a, b = a.cpu().numpy(), b.cpu().numpy()
+        assert np.linalg.norm(a - b) <= 1e-10 * np.linalg.norm(b)
