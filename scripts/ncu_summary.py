@@ -32,7 +32,7 @@ def main(rep, out, note):
     kernels = {}
     for r in rows[2:]:
         d = dict(zip(hdr, r))
-        name = d["Kernel Name"].split("(")[0].split("<")[0]
+        name = d["Kernel Name"].split("(")[0].split("<")[0].replace("void ", "").strip()
         rec = {}
         for m, (key, _) in METRICS.items():
             if m not in d or d[m] == "":

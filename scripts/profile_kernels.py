@@ -15,7 +15,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 warnings.simplefilter("ignore")
 
 import paper_1512_05820_b200 as pk  # noqa: E402
-from paper_1512_05820_b200.linalg import empty_block, gemm_nn, gram, spmm, scale_columns  # noqa: E402
+from paper_1512_05820_b200.linalg import (  # noqa: E402
+    empty_block, gemm_nn, gram, scale_columns, spmm, symmetric_gram_from_products)
 from paper_1512_05820_b200.problems import elasticity_sequence  # noqa: E402
 
 ap = argparse.ArgumentParser()
@@ -48,11 +49,13 @@ try:
 except pk.NotConverged:
     pass
 
-# truncation at the grown width
+# truncation at the grown width: the sequence's Z'AZ from the cached products
+# A Y (stage 1) and A V (stage 3) -- one upper-triangle launch over both segments
 Z = empty_block(A.n, args.grown, dev)
 Z.normal_()
 AZ = spmm(A, Z)
-G = gram(Z, AZ)
+U = symmetric_gram_from_products(Z, [(AZ[:, :60], 0), (AZ[:, 60:], 60)])
+G = gram(Z[:, :256], AZ[:, :256])  # full Gram tile path (128 x 64 tiles)
 C = torch.randn(args.grown, 60, dtype=torch.float64, device=dev)
 Phi = gemm_nn(Z, C)
 torch.cuda.synchronize()
