@@ -139,6 +139,131 @@ def _as_operator(op, sink):
     raise DimensionMismatch("unsupported operator type")
 
 
+class DenseReducedOperator(LinearOperator):
+    """p -> G p with the reduced matrix G = Y'AY already formed (y x y, host).
+
+    Stands in for ReducedSpdOperator (krylov.py:60-83) in the nested reduced
+    solves (stage 2, the phi = 1 inner projection) once Y'AY is known -- the
+    stage-1 Gram when W = Y, otherwise one SpMM + DMMA Gram per system. Every
+    application is charged one matvec to the sink, exactly as the reference's
+    implicit operator, and the reduced products are recorded. Equal to
+    Y'(A(Y p)) up to rounding; an application costs y^2 host flops instead of
+    two N x y GEMVs, an SpMV and a host round trip on the device."""
+
+    def __init__(self, G, sink=None, record_products: bool = False):
+        self.G = np.ascontiguousarray(np.asarray(to_numpy(G), dtype=np.float64))
+        self.dim = int(self.G.shape[0])
+        self.device = None
+        self.sink = sink
+        self.reduced_products: list | None = [] if record_products else None
+
+    def apply(self, p):
+        if self.sink is not None:
+            self.sink.add_matvec()
+        out = self.G @ np.asarray(to_numpy(p), dtype=np.float64)
+        if self.reduced_products is not None:
+            self.reduced_products.append(out)
+        return out
+
+
+def _host_augmented_pcg(op: DenseReducedOperator, b, yhat0, B, reduced_solver, tol, mode, paper_fom_beta,
+                        relative, max_iter, r0, monitor):
+    """augmented_pcg (krylov.py:181-345) for a small dense reduced operator, in
+    host numpy: the same statements in the same order (so the same rounding as
+    the reference's reduced-space arithmetic), no preconditioner. Returns host
+    arrays (V is y x k)."""
+    n = op.dim
+    b = np.asarray(to_numpy(b), dtype=np.float64)
+    if b.shape[0] != n:
+        raise DimensionMismatch("augmented_pcg: rhs length mismatch")
+    Y = None
+    if B is not None:
+        Y = np.asarray(to_numpy(B), dtype=np.float64)
+        if Y.ndim != 2 or Y.shape[0] != n:
+            raise DimensionMismatch("augmented_pcg: basis shape mismatch")
+        if Y.shape[1] == 0:
+            Y = None
+    if Y is not None:
+        if yhat0 is None:
+            raise DimensionMismatch("augmented_pcg: yhat0 required with a nonempty basis")
+        yhat0 = np.asarray(to_numpy(yhat0), dtype=np.float64)
+        if yhat0.shape[0] != Y.shape[1]:
+            raise DimensionMismatch("augmented_pcg: yhat0 length mismatch")
+        x = Y @ yhat0
+        if reduced_solver is None:
+            cross = np.column_stack([op.apply(Y[:, i]) for i in range(Y.shape[1])])
+            g = Y.T @ cross
+            L = dense_cholesky(0.5 * (g + g.T))
+            reduced_solver = lambda z: L.solve_spd(cross.T @ z)  # noqa: E731
+    else:
+        x = np.zeros(n)
+    if r0 is not None:
+        r = np.array(to_numpy(r0), dtype=np.float64)
+    elif Y is not None and np.any(x):
+        r = b - op.apply(x)
+    else:
+        r = b.copy()
+    threshold = tol * np.linalg.norm(b) if relative else tol
+    history = [float(np.linalg.norm(r))]
+    if monitor is not None:
+        monitor(0, x.copy())
+
+    def result(k, alphas, dirs, gammas, converged):
+        return AugmentedPcgResult(k=k, vhat=np.asarray(alphas, dtype=np.float64),
+                                  V=np.column_stack(dirs) if dirs else np.zeros((n, 0)),
+                                  gamma=np.asarray(gammas, dtype=np.float64),
+                                  residual_history=np.asarray(history), x=x, converged=converged)
+
+    if history[0] <= threshold:
+        return result(0, [], [], [], True)
+    if max_iter is None:
+        max_iter = n
+    z = r.copy()
+    p = z - Y @ reduced_solver(z) if Y is not None else z.copy()
+    rz = float(r @ z)
+    alphas, dirs, gammas, a_dirs, rz_hist = [], [], [], [], []
+    for k in range(max_iter):
+        Ap = op.apply(p)
+        gamma = float(p @ Ap)
+        if not np.isfinite(gamma) or gamma <= _BREAKDOWN_RTOL * float(p @ p):
+            raise Breakdown(f"direction curvature {gamma:.3e} at iteration {k}")
+        alpha = rz / gamma
+        x = x + alpha * p
+        r = r - alpha * Ap
+        alphas.append(alpha)
+        dirs.append(p)
+        gammas.append(gamma)
+        rz_hist.append(rz)
+        if mode == "fom":
+            a_dirs.append(Ap)
+        history.append(float(np.linalg.norm(r)))
+        if monitor is not None:
+            monitor(k + 1, x.copy())
+        if history[-1] <= threshold:
+            return result(k + 1, alphas, dirs, gammas, True)
+        z = r.copy()
+        rz_next = float(r @ z)
+        mu = reduced_solver(z) if Y is not None else None
+        if mode == "cg":
+            p = z + (rz_next / rz) * p
+            if Y is not None:
+                p -= Y @ mu
+        elif mode == "fom":
+            p = z - Y @ mu if Y is not None else z.copy()
+            if paper_fom_beta:
+                for i in range(len(dirs)):
+                    p = p + (rz_next / rz_hist[i]) * dirs[i]
+            else:
+                for _ in range(2):
+                    for i in range(len(dirs)):
+                        p = p - (float(a_dirs[i] @ p) / gammas[i]) * dirs[i]
+        else:
+            raise ValueError(f"unknown mode {mode!r}")
+        rz = rz_next
+    raise NotConverged(f"no convergence to {threshold:.3e} within {max_iter} iterations",
+                       partial=result(max_iter, alphas, dirs, gammas, False))
+
+
 class BlockDiagFactor:
     """Cholesky factor of a block-diagonal Gram matrix (krylov.py:97-132):
     dense lower-triangular blocks or square roots of diagonal blocks."""
@@ -399,6 +524,11 @@ def augmented_pcg(
     ``keep_products`` keeps every A p_k as a column of ``result.AV`` (fom mode
     keeps them anyway) so a later POD truncation needs no SpMM.
     """
+    if isinstance(op, DenseReducedOperator):
+        if precond is not None:
+            raise NotImplementedError("a dense reduced operator runs unpreconditioned (as the reference's inner solves)")
+        return _host_augmented_pcg(op, b, yhat0, aug_basis, reduced_solver, tol, mode, paper_fom_beta, relative,
+                                   max_iter, r0, monitor)
     operator = _as_operator(op, sink)
     n = int(operator.dim)
     device = operator.device

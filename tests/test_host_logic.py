@@ -150,3 +150,35 @@ def test_laplacian_and_diffusion_generators():
     seq = diffusion3d_sequence(6, p=2, rtol=1e-4, seed=2, corr_len=2.0)
     A = seq[0].A.to_scipy()
     assert abs(A - A.T).max() < 1e-14 and np.linalg.eigvalsh(A.toarray()).min() > 0
+
+
+@pytest.mark.parametrize("mode", ["cg", "fom"])
+def test_dense_reduced_pcg_matches_oracle(mode):
+    """The y-dimensional nested solves (stage 2, phi = 1) run augmented PCG on
+    a DenseReducedOperator in host numpy: same iterates, vhat, gamma and the
+    same one-matvec-per-application charging as the oracle's restatement of
+    krylov.py:181-345 with the operator p -> G p."""
+    from oracle import recycle_oracle as O
+    from paper_1512_05820_b200.krylov import DenseReducedOperator, augmented_pcg
+
+    rng = np.random.default_rng(5)
+    y = 40
+    M = rng.standard_normal((y, y))
+    G = M @ M.T + y * np.eye(y)
+    B = np.linalg.qr(rng.standard_normal((y, 6)))[0]
+    b = rng.standard_normal(y)
+    yh = np.linalg.solve(B.T @ G @ B, B.T @ b)
+    cross = G @ B
+    L = dense_cholesky(B.T @ cross)
+    sink = InstrumentationSink()
+    op = DenseReducedOperator(G, sink=sink, record_products=True)
+    res = augmented_pcg(op, b, yh, B, lambda z: L.solve_spd(cross.T @ z), None, 1e-10, mode=mode,
+                        r0=b - cross @ yh)
+    t = O.Tally()
+    proj = O.Projection(cross, O.Factor())
+    proj.factor.add_dense(O.cholesky_lower(B.T @ cross))
+    ref = O.aug_pcg(lambda v: (t.__setattr__("matvecs", t.matvecs + 1), G @ v)[1], b, yh, B, proj, None, 1e-10,
+                    mode=mode, r0=b - cross @ yh, tally=t)
+    assert res.k == ref.k and sink.matvecs == res.k == len(op.reduced_products)
+    np.testing.assert_allclose(res.x, ref.x, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(res.gamma, ref.gamma, rtol=1e-12)
