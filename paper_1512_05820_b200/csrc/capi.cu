@@ -359,28 +359,34 @@ int rk_profile_begin(void) {
 // slot (4 slots: spmv, update, finish, direction). Iterations launched after
 // the run had converged (a batch's overshoot: every kernel returns at once) are
 // left out: a sampled iteration counts only when its SpMV took more than a
-// quarter of the longest sampled SpMV.
+// quarter of the 90th-percentile sampled SpMV.
 int rk_profile_end(double* ms4, int64_t* count4) {
   rkh::g_prof.on = false;
   for (int i = 0; i < 4; ++i) { ms4[i] = 0.0; count4[i] = 0; }
   auto& mk = rkh::g_prof.marks;
   if (!mk.empty() && cudaEventSynchronize(mk.back().second) != cudaSuccess) return rkh::cuda_check("rk_profile_end");
-  std::vector<float> dur(mk.size(), -1.f);
-  float longest_spmv = 0.f;
+  std::vector<float> dur(mk.size(), -1.f), spmv;
   for (size_t i = 0; i + 1 < mk.size(); ++i) {
     const int a = mk[i].first, b = mk[i + 1].first;
     if (b == a + 1 && a < 4) {
       float ms = 0.f;
       if (cudaEventElapsedTime(&ms, mk[i].second, mk[i + 1].second) == cudaSuccess) {
         dur[i] = ms;
-        if (a == 0) longest_spmv = std::max(longest_spmv, ms);
+        if (a == 0) spmv.push_back(ms);
       }
     }
+  }
+  // reference SpMV time: the 90th percentile (robust to a cold first launch)
+  float ref = 0.f;
+  if (!spmv.empty()) {
+    const size_t q = (spmv.size() * 9) / 10;
+    std::nth_element(spmv.begin(), spmv.begin() + q, spmv.end());
+    ref = spmv[std::min(q, spmv.size() - 1)];
   }
   bool live = false;
   for (size_t i = 0; i + 1 < mk.size(); ++i) {
     const int a = mk[i].first;
-    if (a == 0) live = dur[i] > 0.25f * longest_spmv;
+    if (a == 0) live = dur[i] > 0.25f * ref;
     if (dur[i] >= 0.f && live) {
       ms4[a] += dur[i];
       count4[a] += 1;
