@@ -646,9 +646,12 @@ __global__ void __launch_bounds__(kSpmvThreads) k_sell1_spmm(const rk_csr A, int
   const int lane = threadIdx.x & 31;
   const int64_t nsl = (A.n + 31) / 32;
   const int64_t wpb = kSpmvThreads / 32;
-  const int64_t c0 = (int64_t)blockIdx.y * CT;
+  // blockIdx.x = column tile, blockIdx.y = slice group: the tiles of one row
+  // range are adjacent in launch order and share the matrix slice and the
+  // gathered neighbour rows in L2
+  const int64_t c0 = (int64_t)blockIdx.x * CT;
   const int ncol = (int)(m - c0 < CT ? m - c0 : CT);
-  for (int64_t sl = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); sl < nsl; sl += (int64_t)gridDim.x * wpb) {
+  for (int64_t sl = (int64_t)blockIdx.y * wpb + (threadIdx.x >> 5); sl < nsl; sl += (int64_t)gridDim.y * wpb) {
     double acc[CT];
 #pragma unroll
     for (int j = 0; j < CT; ++j) acc[j] = 0.0;
@@ -927,8 +930,9 @@ int launch_spmm(const rk_csr& A, int64_t m, const double* X, int64_t ldx, double
     static const int cap = resident_blocks((const void*)rk::k_sell1_spmm<CT>, rk::kSpmvThreads);
     const int64_t tiles = (m + CT - 1) / CT;
     const int64_t need = ((A.n + 31) / 32 + rk::kSpmvThreads / 32 - 1) / (rk::kSpmvThreads / 32);
-    const int64_t gx = std::max<int64_t>(1, std::min<int64_t>(need, std::max<int64_t>(1, cap / tiles)));
-    rk::k_sell1_spmm<CT><<<dim3((unsigned)gx, (unsigned)tiles), rk::kSpmvThreads, 0, s>>>(A, m, X, ldx, Y, ldy);
+    (void)cap;
+    const int64_t gy = std::max<int64_t>(1, std::min<int64_t>(need, 65535));
+    rk::k_sell1_spmm<CT><<<dim3((unsigned)tiles, (unsigned)gy), rk::kSpmvThreads, 0, s>>>(A, m, X, ldx, Y, ldy);
     note_launch();
     return cuda_check("rk_spmm (sell1)");
   }
