@@ -366,6 +366,7 @@ def run_b200(args, rank, world, dist):
             "peak_source": peaks["source"],
         },
         "gram": gram,
+        "pcg_vectors": _pcg_vector_rooflines(n, reports, avg, peaks),
         "kernels_ms_avg": {"spmv_pcg": round(avg[0], 4), "pcg_update": round(avg[1], 4),
                            "pcg_finish": round(avg[2], 4), "pcg_direction": round(avg[3], 4),
                            "launches": list(cnt)},
@@ -383,6 +384,28 @@ def run_b200(args, rank, world, dist):
         with open(os.path.join(ROOT, "gpurun_out", f"{args.workload}_schedule.json"), "w") as fh:
             json.dump(sched, fh)
     return line, host_specs, sched
+
+
+def _pcg_vector_rooflines(n, reports, avg, peaks):
+    """SURVEY 8d's fused-PCG GB/s: algorithmic bytes of the update kernel
+    ((5 + m) 8N read + 3 * 8N written: x, p, r, Ap, 1/diag and the m columns of
+    cross; x, r, z) and of the direction kernel ((3 + m) 8N: z, p_k and the m
+    columns of B read, p_{k+1} written), averaged over the run's iterations
+    with each system's projection width m, over the CUDA-event durations."""
+    iters = [r.stage3_iters for r in reports]
+    widths = [r.basis_dim if r.basis_dim else 0 for r in reports]
+    tot = max(sum(iters), 1)
+    upd = sum(k * (8 + w) * 8 * n for k, w in zip(iters, widths)) / tot
+    dirb = sum(k * (3 + w) * 8 * n for k, w in zip(iters, widths)) / tot
+    out = {}
+    # avg[1]: the update kernel with its fused finish (widths <= 64; wider runs add
+    # k_pcg_finish + k_pcg_musolve, sampled separately in avg[2])
+    for name, b, ms in (("update", upd, avg[1]), ("direction", dirb, avg[3])):
+        if ms > 0:
+            gbs = b / (ms * 1e-3) / 1e9
+            out[name] = {"algorithmic_bytes_per_launch": int(b), "avg_launch_ms": round(ms, 4),
+                         "achieved_GB_s": round(gbs, 1), "frac": round(gbs / peaks["hbm_gbs"], 3)}
+    return out
 
 
 DMMA_PEAK_TFLOPS = 37.1  # B200 FP64 tensor (DMMA) peak measured by scripts/dmma_probe.cu (profiles/dmma_peak_r01.json)
