@@ -1,0 +1,85 @@
+"""Size-independent properties at BASELINE's full sizes, where the oracle
+would take minutes per system: the solver's exit residual is the true
+residual, every run converged within the reference's tolerance, the
+truncated POD basis is A-orthonormal (Phi' A Phi = I), and the C5 POD
+basis reconstructs the snapshot energy."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pk():
+    import paper_1512_05820_b200 as pk
+
+    return pk
+
+
+def _true_residual(A_host, b, x):
+    import scipy.sparse
+
+    As = scipy.sparse.csr_matrix((A_host.values, A_host.col_indices, A_host.row_offsets), shape=(A_host.n,) * 2)
+    return float(np.linalg.norm(b - As @ x))
+
+
+@pytest.mark.parametrize("workload", ["c3", "c2"])
+def test_full_size_sequence_residuals_and_basis(pk, workload):
+    """C3 (811,200 DOF Q1 elasticity, 3x3-block SELL) and C2 (2.1M-row
+    diffusion, scalar SELL), first 3 systems at full size: each x meets
+    ||b - A x|| <= tol (checked on the host with scipy, independent of the
+    device residual recurrence, allowing the recurrence/true-residual drift
+    of 1e-3 relative the reference also has), and after every truncation the
+    new basis is A-orthonormal (leading 10 modes) to 1e-9."""
+    from paper_1512_05820_b200.problems import diffusion3d_sequence, elasticity_sequence
+    from paper_1512_05820_b200.linalg import assemble_gram
+
+    if workload == "c3":
+        seq, cap = elasticity_sequence((64, 64, 64), p=3, rtol=1e-5, seed=3), 60
+    else:
+        seq, cap = diffusion3d_sequence(128, p=3, rtol=1e-4, seed=2), 40
+    specs = list(seq)
+    cfg = pk.SolverConfig(truncation=pk.TruncationConfig(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0,
+                                                         storage_cap=cap, max_dim=cap), mode="cg")
+    state = pk.RecycleState.empty(seq.n, torch.device("cuda", 0))
+    for j, s in enumerate(specs):
+        A = pk.SparseSpdMatrix.from_host(s.A)
+        M = pk.build_preconditioner("jacobi", A)
+        x, rep, state = pk.solve_system(A, s.b, None, state, pk.StageTolerances(eps=s.tol), cfg, M=M)
+        assert rep.converged and rep.stage3_iters > 0
+        res = _true_residual(s.A, s.b, x.cpu().numpy())
+        assert res <= s.tol * (1 + 1e-3), (j, res, s.tol)
+        if rep.truncated:
+            # leading modes (the trailing ones carry sigma_1 / sigma_i rounding amplification)
+            G, _ = assemble_gram(A, state.Y[:, :10])
+            G = G.cpu().numpy()
+            assert np.abs(G - np.eye(G.shape[0])).max() <= 1e-9
+
+
+def test_c5_full_size_pod_properties(pk):
+    """C5 shape (7-point Laplacian on 128x128x256, N = 4,194,304) with 64
+    Gaussian snapshots: the column-blocked Gram is symmetric positive, the POD
+    basis is A-orthonormal and reproduces S in the A-norm (sum of sigma^2 =
+    trace of the Gram)."""
+    from paper_1512_05820_b200.linalg import assemble_gram, empty_block
+    from paper_1512_05820_b200.problems import laplacian3d
+
+    L = laplacian3d(128, 128, 256)
+    A = pk.SparseSpdMatrix(L.n, L.row_offsets, L.col_indices, L.values)
+    S = empty_block(L.n, 64, "cuda")
+    S.normal_(generator=torch.Generator(device="cuda").manual_seed(5))
+    G = pk.assemble_gram_blocked(A, S, block=40)
+    Gh = np.asarray(G)
+    Gf, _ = assemble_gram(A, S)
+    np.testing.assert_allclose(Gh, Gf.cpu().numpy(), rtol=0, atol=1e-11 * np.abs(Gh).max())
+    import warnings
+
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        res = pk.pod_evd_from_gram(G, S, np.ones(64), 1.0)
+    Phi = res.columns
+    P, _ = assemble_gram(A, Phi)
+    assert np.abs(P.cpu().numpy() - np.eye(Phi.shape[1])).max() <= 1e-12
+    np.testing.assert_allclose(np.sum(res.singular_values ** 2), np.trace(Gh), rtol=1e-12)
