@@ -236,3 +236,43 @@ def test_invariant_matrix_stage1_reuses_products(pk):
     for a, b in zip(xs_a, xs_b):
         a, b = a.cpu().numpy(), b.cpu().numpy()
         assert np.linalg.norm(a - b) <= 1e-10 * np.linalg.norm(b)
+
+
+def test_copied_state_never_writes_into_shared_storage(pk):
+    """RecycleState grows Y and reuses A W storage in place; a shallow copy
+    (copy.copy) shares those tensors but must not write into them: two
+    branches continued from a copy give bitwise the results of branches
+    continued from a deep copy."""
+    import copy
+
+    from paper_1512_05820_b200.problems import poisson2d_sequence
+
+    specs = list(poisson2d_sequence(32, p=6))
+    A = pk.SparseSpdMatrix.from_host(specs[0].A)
+    M = pk.build_preconditioner("jacobi", A)
+    cfg = pk.SolverConfig(truncation=pk.TruncationConfig(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0,
+                                                         storage_cap=1000, max_dim=60), mode="cg")
+    tol = pk.StageTolerances(eps=specs[0].tol)
+
+    def branch_pair(shallow):
+        st = pk.RecycleState.empty(A.n, A.device)
+        for s in specs[:2]:
+            _, _, st = pk.solve_system(A, s.b, None, st, tol, cfg, M=M)
+        if shallow:
+            other = copy.copy(st)
+        else:
+            other = pk.RecycleState(n=st.n, Y=st.Y.clone(), stage1_idx=list(st.stage1_idx),
+                                    last_trunc_index=st.last_trunc_index, systems_seen=st.systems_seen)
+        other.history = copy.deepcopy(st.history)
+        other.stage1_idx = list(st.stage1_idx)
+        xs = []
+        for a, b in ((specs[2], specs[3]), (specs[4], specs[5])):
+            xa, _, st = pk.solve_system(A, a.b, None, st, tol, cfg, M=M)
+            xb, _, other = pk.solve_system(A, b.b, None, other, tol, cfg, M=M)
+            xs += [xa.cpu().numpy(), xb.cpu().numpy()]
+        return xs
+
+    deep = branch_pair(False)
+    shallow = branch_pair(True)
+    for u, v in zip(deep, shallow):
+        assert np.array_equal(u, v)
