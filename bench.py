@@ -108,7 +108,7 @@ def workload_config(args, n=None, nnz=None):
         "rtol": w["rtol"],
         "truncation": f"pod-a-rbf nu_y=1 nu_w=1 storage_cap={w['cap']} max_dim={w.get('max_dim', w['cap'])}",
         "l2": w["l2"],
-        "parallelism": "replicas (one independent sequence per GPU)",
+        "parallelism": "replicas (the same seeded sequence solved independently on every GPU)",
     }
 
 
@@ -226,6 +226,45 @@ def bsr3_bytes(n, nblk):
     return 76 * nblk + 4 * (n // 3 + 1) + 16 * n
 
 
+def _shared_host_specs(args, seq, rank, world, dist):
+    """The sequence's host arrays. With N > 1 replicas every rank solves the
+    same seeded sequence; rank 0 generates it once into a file that all ranks
+    map read-only, so the host holds one copy (C3: 20.6 GB of values) instead
+    of one per rank (8 ranks would need ~170 GB of the box's host memory)."""
+    if world <= 1:
+        return list(seq)
+    from paper_1512_05820_b200.problems import HostCsr, LinearSystemSpec
+
+    base = os.path.join(os.environ.get("RK_BENCH_SHM", "/tmp"), f"rk_bench_{args.workload}_{args.grid}_{args.systems}")
+    if rank == 0:
+        specs = list(seq)
+        uniq = []
+        for s_ in specs:
+            if not any(s_.A is u for u in uniq):
+                uniq.append(s_.A)
+        np.save(base + "_rp.npy", np.asarray(uniq[0].row_offsets))
+        np.save(base + "_ci.npy", np.asarray(uniq[0].col_indices))
+        vals = np.lib.format.open_memmap(base + "_vals.npy", mode="w+", dtype=np.float64,
+                                         shape=(len(uniq), uniq[0].nnz))
+        for i, u in enumerate(uniq):
+            vals[i] = u.values
+        vals.flush()
+        which = np.array([next(i for i, u in enumerate(uniq) if s_.A is u) for s_ in specs])
+        np.save(base + "_which.npy", which)
+        np.save(base + "_b.npy", np.stack([s_.b for s_ in specs]))
+        np.save(base + "_tol.npy", np.array([s_.tol for s_ in specs]))
+        del specs, uniq, vals
+    barrier(dist)
+    rp = np.load(base + "_rp.npy", mmap_mode="r")
+    ci = np.load(base + "_ci.npy", mmap_mode="r")
+    vals = np.load(base + "_vals.npy", mmap_mode="r")
+    which = np.load(base + "_which.npy")
+    bs = np.load(base + "_b.npy", mmap_mode="r")
+    tols = np.load(base + "_tol.npy")
+    mats = [HostCsr(seq.n, rp, ci, vals[i]) for i in range(vals.shape[0])]
+    return [LinearSystemSpec(A=mats[w], b=bs[j], xbar=None, tol=float(tols[j])) for j, w in enumerate(which)]
+
+
 def run_b200(args, rank, world, dist):
     import torch
 
@@ -235,8 +274,8 @@ def run_b200(args, rank, world, dist):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     lib = nat.lib()
-    seq = make_sequence(args, seed_offset=rank)
-    host_specs = list(seq)  # host CSR values + rhs for every system (the e2e inputs)
+    seq = make_sequence(args, seed_offset=0 if world > 1 else rank)
+    host_specs = _shared_host_specs(args, seq, rank, world, dist)  # host CSR values + rhs (the e2e inputs)
     n = seq.n
     nnz = host_specs[0].A.nnz
     # device-resident inputs for `value`
@@ -246,7 +285,7 @@ def run_b200(args, rank, world, dist):
         if id(s.A) not in uploaded:
             uploaded[id(s.A)] = pk.SparseSpdMatrix.from_host(s.A)
         A = uploaded[id(s.A)]
-        dev_specs.append(pk.LinearSystemSpec(A=A, b=torch.from_numpy(s.b).to(dev), xbar=None, tol=s.tol))
+        dev_specs.append(pk.LinearSystemSpec(A=A, b=torch.from_numpy(np.array(s.b)).to(dev), xbar=None, tol=s.tol))
     dseq = pk.SystemSequence(n, dev_specs, C=seq.C)
     cfg = solver_config(pk, args)
     jac = lambda A: pk.build_preconditioner("jacobi", A)  # noqa: E731
