@@ -241,6 +241,43 @@ def run_c3_mid(rk):
     return {"c3_mid": d}
 
 
+def run_c3_full(rk, p=2):
+    """The bench's own C3 workload at full size (64^3 Q1 elasticity, N =
+    811,200), its first p systems through the reference itself (CG, cap =
+    max_dim = 60): counters, q = c'x, ||x|| and x at 2000 fixed indices (the
+    full vectors would be 6.5 MB each; the test regenerates the inputs from
+    the seeded generator)."""
+    from recykl import preconditioners
+    from recykl.threestage import SolverConfig, run_sequence
+    from recykl.truncation import TruncationConfig
+
+    from paper_1512_05820_b200.problems import elasticity_sequence
+
+    mine = elasticity_sequence((64, 64, 64), p=p, rtol=1e-5, seed=3)
+    specs, seq = _ref_sequence(mine)
+    idx = np.sort(np.random.default_rng(0).choice(mine.n, 2000, replace=False))
+    d = {"n": np.int64(mine.n), "p": np.int64(p), "idx": idx}
+    cfg = SolverConfig(truncation=TruncationConfig(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=60,
+                                                   max_dim=60), mode="cg")
+    xs, reps, _ = run_sequence(seq, cfg, precond_factory=lambda M: preconditioners.build("jacobi", M))
+    for key in ("stage3_iters", "matvecs", "precond_applies", "final_residual", "truncated", "converged"):
+        d[f"cg_{key}"] = np.asarray([getattr(r, key) for r in reps])
+    for j, x in enumerate(xs, start=1):
+        d[f"cg_q{j}"] = np.float64(mine.C[0] @ x)
+        d[f"cg_xnorm{j}"] = np.float64(np.linalg.norm(x))
+        d[f"cg_xs{j}"] = np.asarray(x, dtype=np.float64)[idx]
+    # the reference's own rounding envelope at this size: every right-hand side
+    # scaled by (1 + 1e-15), same everything else
+    for s in seq.systems:
+        s.b = s.b * (1 + 1e-15)
+    xs2, reps2, _ = run_sequence(seq, cfg, precond_factory=lambda M: preconditioners.build("jacobi", M))
+    d["pert_stage3_iters"] = np.asarray([r.stage3_iters for r in reps2])
+    for j, (x, x2) in enumerate(zip(xs, xs2), start=1):
+        d[f"pert_q{j}"] = np.float64(mine.C[0] @ x2)
+        d[f"pert_xrel{j}"] = np.float64(np.linalg.norm(x2 - x) / np.linalg.norm(x))
+    return {"c3_full": d}
+
+
 def run_c5_small(rk):
     """C5 microbench at reduced size: Laplacian 16x16x32, Gaussian S with 256
     columns, gamma = 1: assemble_gram + pod_evd_from_gram (nu = 1)."""
@@ -413,9 +450,9 @@ def main():
     blobs = {}
     only = sys.argv[1:]
     runs = [run_fixture_cases, run_stage_variants, run_kernels, run_elasticity, run_c1, run_c2_small, run_c3_mid,
-            run_c5_small, run_next_strategies, run_manifest]
+            run_c5_small, run_next_strategies, run_manifest, run_c3_full]
     for fn in runs:
-        if not only or fn.__name__ in only:
+        if (not only and fn is not run_c3_full) or fn.__name__ in only:  # c3_full (minutes) only by name
             blobs.update(fn(rk))
     for name, d in blobs.items():
         path = os.path.join(OUT, f"{name}.npz")

@@ -21,6 +21,24 @@ namespace rk {
 
 constexpr int kSpmvThreads = 256;
 
+// Row-sum step of every SpMV / SpMM kernel: a separately rounded multiply and
+// add, entries in CSR order, so a SELL row sum is scipy's csr_matvec loop
+// `sum += Ax[jj] * Xx[Aj[jj]]` (linalg.py:148) bit for bit. Measured at full
+// C3 size against the reference: with fused multiply-adds the first system
+// took 746 iterations instead of the reference's 748 (x off by 4.5e-8); with
+// the scipy arithmetic 748 (x within 1.3e-9), at no cost in a memory-bound
+// kernel. RK_SPMV_FMA=1 builds the fused variant.
+#ifndef RK_SPMV_FMA
+#define RK_SPMV_FMA 0
+#endif
+__device__ __forceinline__ double row_madd(double a, double b, double s) {
+#if RK_SPMV_FMA
+  return fma(a, b, s);
+#else
+  return __dadd_rn(s, __dmul_rn(a, b));
+#endif
+}
+
 // Entries per lane per pass for each group width: LANES * U covers the
 // typical row in one pass (2 x 4 = 8 for 7-point rows, 16 x 6 = 96 for the
 // 81-entry Q1 elasticity rows).
@@ -56,7 +74,7 @@ __device__ __forceinline__ double csr_row_dot(const int32_t* __restrict__ rp,
 #pragma unroll
       for (int u = 0; u < U; ++u) xv[u] = __ldg(x + c[u]);
 #pragma unroll
-      for (int u = 0; u < U; ++u) s = fma(v[u], xv[u], s);
+      for (int u = 0; u < U; ++u) s = row_madd(v[u], xv[u], s);
     }
   }
 #pragma unroll
@@ -185,7 +203,7 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmm(int64_t n, const int32_t*
         const double* xc = X + (int64_t)__ldg(ci + j) + c0 * ldx;
 #pragma unroll
         for (int t = 0; t < CT; ++t)
-          if (t < ct) acc[t] = fma(v, __ldg(xc + t * ldx), acc[t]);
+          if (t < ct) acc[t] = row_madd(v, __ldg(xc + t * ldx), acc[t]);
       }
     }
 #pragma unroll
@@ -322,9 +340,9 @@ __device__ __forceinline__ void sell3_row_pipe(const rk_csr& A, const double* __
 #pragma unroll
       for (int e = 0; e < 9; ++e) v2[e] = __ldcs(val + 288 * (t + 2) + 32 * e);
     }
-    s0 = fma(v0[0], x0[0], s0); s0 = fma(v0[1], x0[1], s0); s0 = fma(v0[2], x0[2], s0);
-    s1 = fma(v0[3], x0[0], s1); s1 = fma(v0[4], x0[1], s1); s1 = fma(v0[5], x0[2], s1);
-    s2 = fma(v0[6], x0[0], s2); s2 = fma(v0[7], x0[1], s2); s2 = fma(v0[8], x0[2], s2);
+    s0 = row_madd(v0[0], x0[0], s0); s0 = row_madd(v0[1], x0[1], s0); s0 = row_madd(v0[2], x0[2], s0);
+    s1 = row_madd(v0[3], x0[0], s1); s1 = row_madd(v0[4], x0[1], s1); s1 = row_madd(v0[5], x0[2], s1);
+    s2 = row_madd(v0[6], x0[0], s2); s2 = row_madd(v0[7], x0[1], s2); s2 = row_madd(v0[8], x0[2], s2);
 #pragma unroll
     for (int e = 0; e < 9; ++e) {
       v0[e] = v1[e];
@@ -377,9 +395,9 @@ __device__ __forceinline__ void sell3_row_issue(const rk_csr& A, const double* _
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      s0 = fma(v[u][0], xs[u][0], s0); s0 = fma(v[u][1], xs[u][1], s0); s0 = fma(v[u][2], xs[u][2], s0);
-      s1 = fma(v[u][3], xs[u][0], s1); s1 = fma(v[u][4], xs[u][1], s1); s1 = fma(v[u][5], xs[u][2], s1);
-      s2 = fma(v[u][6], xs[u][0], s2); s2 = fma(v[u][7], xs[u][1], s2); s2 = fma(v[u][8], xs[u][2], s2);
+      s0 = row_madd(v[u][0], xs[u][0], s0); s0 = row_madd(v[u][1], xs[u][1], s0); s0 = row_madd(v[u][2], xs[u][2], s0);
+      s1 = row_madd(v[u][3], xs[u][0], s1); s1 = row_madd(v[u][4], xs[u][1], s1); s1 = row_madd(v[u][5], xs[u][2], s1);
+      s2 = row_madd(v[u][6], xs[u][0], s2); s2 = row_madd(v[u][7], xs[u][1], s2); s2 = row_madd(v[u][8], xs[u][2], s2);
     }
   }
   for (; t < width; ++t) {
@@ -389,9 +407,9 @@ __device__ __forceinline__ void sell3_row_issue(const rk_csr& A, const double* _
     for (int e = 0; e < 9; ++e) va[e] = ld_stream_f64(val + 288 * t + 32 * e);
     const double* xa = x + 3 * (int64_t)ca;
     const double a0 = __ldg(xa), a1 = __ldg(xa + 1), a2 = __ldg(xa + 2);
-    s0 = fma(va[0], a0, s0); s0 = fma(va[1], a1, s0); s0 = fma(va[2], a2, s0);
-    s1 = fma(va[3], a0, s1); s1 = fma(va[4], a1, s1); s1 = fma(va[5], a2, s1);
-    s2 = fma(va[6], a0, s2); s2 = fma(va[7], a1, s2); s2 = fma(va[8], a2, s2);
+    s0 = row_madd(va[0], a0, s0); s0 = row_madd(va[1], a1, s0); s0 = row_madd(va[2], a2, s0);
+    s1 = row_madd(va[3], a0, s1); s1 = row_madd(va[4], a1, s1); s1 = row_madd(va[5], a2, s1);
+    s2 = row_madd(va[6], a0, s2); s2 = row_madd(va[7], a1, s2); s2 = row_madd(va[8], a2, s2);
   }
 }
 
@@ -424,9 +442,9 @@ __device__ __forceinline__ void sell3_row(const rk_csr& A, const double* __restr
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {  // slots in order: the same fma chain for every U
-      s0 = fma(v[u][0], xs[u][0], s0); s0 = fma(v[u][1], xs[u][1], s0); s0 = fma(v[u][2], xs[u][2], s0);
-      s1 = fma(v[u][3], xs[u][0], s1); s1 = fma(v[u][4], xs[u][1], s1); s1 = fma(v[u][5], xs[u][2], s1);
-      s2 = fma(v[u][6], xs[u][0], s2); s2 = fma(v[u][7], xs[u][1], s2); s2 = fma(v[u][8], xs[u][2], s2);
+      s0 = row_madd(v[u][0], xs[u][0], s0); s0 = row_madd(v[u][1], xs[u][1], s0); s0 = row_madd(v[u][2], xs[u][2], s0);
+      s1 = row_madd(v[u][3], xs[u][0], s1); s1 = row_madd(v[u][4], xs[u][1], s1); s1 = row_madd(v[u][5], xs[u][2], s1);
+      s2 = row_madd(v[u][6], xs[u][0], s2); s2 = row_madd(v[u][7], xs[u][1], s2); s2 = row_madd(v[u][8], xs[u][2], s2);
     }
   }
   for (; t < width; ++t) {
@@ -436,9 +454,9 @@ __device__ __forceinline__ void sell3_row(const rk_csr& A, const double* __restr
     for (int e = 0; e < 9; ++e) va[e] = __ldcs(val + 288 * t + 32 * e);
     const double* xa = x + 3 * (int64_t)ca;
     const double a0 = __ldg(xa), a1 = __ldg(xa + 1), a2 = __ldg(xa + 2);
-    s0 = fma(va[0], a0, s0); s0 = fma(va[1], a1, s0); s0 = fma(va[2], a2, s0);
-    s1 = fma(va[3], a0, s1); s1 = fma(va[4], a1, s1); s1 = fma(va[5], a2, s1);
-    s2 = fma(va[6], a0, s2); s2 = fma(va[7], a1, s2); s2 = fma(va[8], a2, s2);
+    s0 = row_madd(va[0], a0, s0); s0 = row_madd(va[1], a1, s0); s0 = row_madd(va[2], a2, s0);
+    s1 = row_madd(va[3], a0, s1); s1 = row_madd(va[4], a1, s1); s1 = row_madd(va[5], a2, s1);
+    s2 = row_madd(va[6], a0, s2); s2 = row_madd(va[7], a1, s2); s2 = row_madd(va[8], a2, s2);
   }
 }
 
@@ -538,9 +556,9 @@ __global__ void __launch_bounds__(kSpmvThreads) k_bsr3_spmm(const rk_csr A, int6
       for (int j = 0; j < CT; ++j) {
         if (j < ncol) {
           const double x0 = __ldg(xc + j * ldx), x1 = __ldg(xc + j * ldx + 1), x2 = __ldg(xc + j * ldx + 2);
-          acc[0][j] = fma(v[0], x0, acc[0][j]); acc[0][j] = fma(v[1], x1, acc[0][j]); acc[0][j] = fma(v[2], x2, acc[0][j]);
-          acc[1][j] = fma(v[3], x0, acc[1][j]); acc[1][j] = fma(v[4], x1, acc[1][j]); acc[1][j] = fma(v[5], x2, acc[1][j]);
-          acc[2][j] = fma(v[6], x0, acc[2][j]); acc[2][j] = fma(v[7], x1, acc[2][j]); acc[2][j] = fma(v[8], x2, acc[2][j]);
+          acc[0][j] = row_madd(v[0], x0, acc[0][j]); acc[0][j] = row_madd(v[1], x1, acc[0][j]); acc[0][j] = row_madd(v[2], x2, acc[0][j]);
+          acc[1][j] = row_madd(v[3], x0, acc[1][j]); acc[1][j] = row_madd(v[4], x1, acc[1][j]); acc[1][j] = row_madd(v[5], x2, acc[1][j]);
+          acc[2][j] = row_madd(v[6], x0, acc[2][j]); acc[2][j] = row_madd(v[7], x1, acc[2][j]); acc[2][j] = row_madd(v[8], x2, acc[2][j]);
         }
       }
     }
@@ -588,7 +606,7 @@ __device__ __forceinline__ double sell1_row(const rk_csr& A, const double* __res
     for (int u = 0; u < U; ++u) xs[u] = __ldg(x + c[u]);
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (t + u < width) s = fma(v[u], xs[u], s);
+      if (t + u < width) s = row_madd(v[u], xs[u], s);
   }
   return s;
 }
@@ -677,7 +695,7 @@ __global__ void __launch_bounds__(kSpmvThreads) k_sell1_spmm(const rk_csr A, int
           for (int u = 0; u < kSell1U; ++u) xs[u] = __ldg(xc + c[u]);
 #pragma unroll
           for (int u = 0; u < kSell1U; ++u)
-            if (t + u < width) acc[j] = fma(v[u], xs[u], acc[j]);
+            if (t + u < width) acc[j] = row_madd(v[u], xs[u], acc[j]);
         }
       }
     }
