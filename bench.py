@@ -56,13 +56,16 @@ def parse():
     ap.add_argument("--grid", type=int, default=64)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--workload", default="c3", choices=["c3", "c2", "c4", "c5"],
-                    help="c3 (default, the north-star sequence), c2 (128^3 diffusion sequence), "
+    ap.add_argument("--workload", default="c3", choices=["c3", "c1", "c2", "c4", "c5"],
+                    help="c3 (default, the north-star sequence), c1 (64x64 Poisson, latency-bound), "
+                         "c2 (128^3 diffusion sequence), "
                          "c4 (128x128x64 dynamic elasticity, snapshot to ~3000), c5 (POD truncation microbench)")
     ap.add_argument("--m", type=int, default=2048, help="c5: snapshot columns")
     args = ap.parse_args()
     if args.workload == "c2" and args.systems == 40:
         args.systems = 30
+    if args.workload == "c1" and args.systems == 40:
+        args.systems = 20
     if args.workload == "c4" and args.systems == 40:
         args.systems = 60
     return args
@@ -72,6 +75,8 @@ def parse():
 WORKLOADS = {
     "c3": {"rtol": 1e-5, "cap": 60, "data": "synthetic (seeded C3 generator, BASELINE configs[2] shapes)",
            "l2": "inputs larger than L2 (552 MB of 3x3-block matrix streamed per SpMV, 20 GB of matrices); no flush"},
+    "c1": {"rtol": 1e-6, "cap": 20, "data": "synthetic (seeded C1 recipe, BASELINE configs[0])",
+           "l2": "latency-bound: the 324 KB matrix and every vector stay in L2 (reported as us per iteration)"},
     "c2": {"rtol": 1e-4, "cap": 40, "data": "synthetic (seeded C2 generator, BASELINE configs[1] shapes)",
            "l2": "inputs larger than L2 (175 MB of CSR streamed per SpMV, 3.5 GB of matrices); no flush"},
     # C4: the snapshot accumulates Krylov vectors up to the storage cap (SURVEY 8d flags cap ~ 3000 as a
@@ -86,6 +91,10 @@ def make_sequence(args, seed_offset=0, p=None):
     from paper_1512_05820_b200.problems import diffusion3d_sequence, elasticity_sequence
 
     p = args.systems if p is None else p
+    if args.workload == "c1":
+        from paper_1512_05820_b200.problems import poisson2d_sequence
+
+        return poisson2d_sequence(64, p=p, rtol=1e-6, seed=0 + seed_offset)
     if args.workload == "c2":
         return diffusion3d_sequence(128, p=p, rtol=1e-4, seed=2 + seed_offset)
     if args.workload == "c4":
@@ -95,7 +104,8 @@ def make_sequence(args, seed_offset=0, p=None):
 
 def workload_config(args, n=None, nnz=None):
     w = WORKLOADS[args.workload]
-    name = {"c2": f"C2 variable-coefficient diffusion 128^3, {args.systems}-system recycled sequence",
+    name = {"c1": f"C1 2-D Poisson 64x64, {args.systems}-system recycled sequence",
+            "c2": f"C2 variable-coefficient diffusion 128^3, {args.systems}-system recycled sequence",
             "c4": f"C4 Q1 elasticity 128x128x64 elements, K + M/dt^2, {args.systems}-system recycled sequence",
             }.get(args.workload, f"C3 Q1 elasticity {args.grid}^3 elements, {args.systems}-system recycled sequence")
     return {
@@ -364,7 +374,7 @@ def run_b200(args, rank, world, dist):
                "path": "run_sequence over host CSR (reference-style SparseSpdMatrix fields), solutions copied back"}
         del xh
 
-    ach = alg_bytes / (avg[0] * 1e-3) / 1e9
+    ach = alg_bytes / (avg[0] * 1e-3) / 1e9 if avg[0] > 0 else None  # C1: single-CTA batches, no per-kernel samples
     traffic = None
     if args.workload == "c3":  # the committed ncu capture is of the C3 SELL kernel
         try:
@@ -394,10 +404,10 @@ def run_b200(args, rank, world, dist):
             "kernel": "K1 SpMV fused with p'Ap, p'p (k_bsr3_spmv_pcg / k_spmv_pcg)",
             "format": fmt,
             "bound": "hbm",
-            "achieved": round(ach, 1),
+            "achieved": round(ach, 1) if ach else None,
             "peak": peaks["hbm_gbs"],
             "unit": "GB/s",
-            "frac": round(ach / peaks["hbm_gbs"], 3),
+            "frac": round(ach / peaks["hbm_gbs"], 3) if ach else None,
             "traffic": traffic,
             "algorithmic_bytes_per_launch": alg_bytes,
             "csr_equivalent_bytes": spmv_bytes(n, nnz),
@@ -410,6 +420,7 @@ def run_b200(args, rank, world, dist):
                            "pcg_finish": round(avg[2], 4), "pcg_direction": round(avg[3], 4),
                            "launches": list(cnt)},
         "sequence": {"stage3_iters_total": int(sum(iters)), "cg_iters_per_s": round(sum(iters) / t_step, 1),
+                     "us_per_iteration": round(t_step / max(sum(iters), 1) * 1e6, 2),
                      "per_system_iters": iters, "q_last": q_last,
                      "all_converged": bool(all(r.converged for r in reports))},
         "e2e": e2e,
@@ -808,12 +819,36 @@ def cpu_sample(host_specs, sched, cap=60, label="C3", budget_s=20.0):
     }
 
 
+def cpu_full_sequence(args):
+    """C1: the oracle port runs the whole sequence (seconds), no extrapolation."""
+    from oracle import recycle_oracle as O
+
+    seq = make_sequence(args)
+    cap = WORKLOADS[args.workload]["cap"]
+    ocfg = O.Config(mode=args.mode, strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=cap, max_dim=cap)
+    O.run_sequence(make_sequence(args, p=2), ocfg, precond="jacobi")  # warm-up
+    t0 = time.perf_counter()
+    _, reps, _ = O.run_sequence(seq, ocfg, precond="jacobi")
+    t = time.perf_counter() - t0
+    return {"value": round(t, 4), "unit": UNIT, "cores": len(os.sched_getaffinity(0)), "kind": "port",
+            "sample": f"the whole {args.systems}-system C1 sequence through the oracle (numpy/scipy as the reference)"}
+
+
 def run_reference(args, rank, world):
     """--impl reference: the oracle port on the box's host cores (rank 0 only)."""
     if rank != 0:
         return None
     if args.workload == "c5":
         return run_reference_c5(args, world)
+    if args.workload == "c1":
+        vals = [cpu_full_sequence(args)["value"] for _ in range(max(args.steps, 1))]
+        cb = cpu_full_sequence(args)
+        cb["value"] = round(float(np.mean(vals)), 4)
+        return {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "higher_is_better": False, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": WORKLOADS["c1"]["data"],
+                "config": workload_config(args, 4096, 20224), "cpu_baseline": cb,
+                "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     seq = make_sequence(args, p=1)
     host_specs = list(seq)
     try:
@@ -875,8 +910,11 @@ def main():
     line, host_specs, sched = run_b200(args, rank, world, dist)
     if rank == 0:
         if world == 1 and not args.no_cpu:
-            line["cpu_baseline"] = cpu_sample(host_specs, sched, WORKLOADS[args.workload]["cap"],
-                                              args.workload.upper())
+            if args.workload == "c1":
+                line["cpu_baseline"] = cpu_full_sequence(args)
+            else:
+                line["cpu_baseline"] = cpu_sample(host_specs, sched, WORKLOADS[args.workload]["cap"],
+                                                  args.workload.upper())
         print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()

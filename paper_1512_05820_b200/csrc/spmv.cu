@@ -21,23 +21,6 @@ namespace rk {
 
 constexpr int kSpmvThreads = 256;
 
-// Row-sum step of every SpMV / SpMM kernel: a separately rounded multiply and
-// add, entries in CSR order, so a SELL row sum is scipy's csr_matvec loop
-// `sum += Ax[jj] * Xx[Aj[jj]]` (linalg.py:148) bit for bit. Measured at full
-// C3 size against the reference: with fused multiply-adds the first system
-// took 746 iterations instead of the reference's 748 (x off by 4.5e-8); with
-// the scipy arithmetic 748 (x within 1.3e-9), at no cost in a memory-bound
-// kernel. RK_SPMV_FMA=1 builds the fused variant.
-#ifndef RK_SPMV_FMA
-#define RK_SPMV_FMA 0
-#endif
-__device__ __forceinline__ double row_madd(double a, double b, double s) {
-#if RK_SPMV_FMA
-  return fma(a, b, s);
-#else
-  return __dadd_rn(s, __dmul_rn(a, b));
-#endif
-}
 
 // Entries per lane per pass for each group width: LANES * U covers the
 // typical row in one pass (2 x 4 = 8 for 7-point rows, 16 x 6 = 96 for the
@@ -96,27 +79,6 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(int64_t n, const int32_t*
     const double s = csr_row_dot<LANES>(rp, ci, val, x, row, valid, sub);
     if (valid && sub == 0) y[row] = s;
   }
-}
-
-// Breakdown test and step length of one iteration (krylov.py:302-305); run by
-// the single last block once gamma = p'Ap and p'p are known.
-__device__ __forceinline__ void curvature_epilogue(const rk_pcg_plan& P, double gamma, double pp) {
-  rk_pcg_state* st = P.st;
-  const int64_t k = st->k;
-  st->gamma = gamma;
-  st->pp = pp;
-  // krylov.py:303  `not isfinite(gamma) or gamma <= 1e-14 * (p @ p)`
-  if (!isfinite(gamma) || gamma <= 1e-14 * pp) {
-    st->status = 2;
-    st->bd_iter = k;
-    st->done = 1;
-    return;
-  }
-  const double alpha = st->rz / gamma;
-  st->alpha = alpha;
-  P.alpha_h[k] = alpha;
-  P.gamma_h[k] = gamma;
-  P.rz_h[k] = st->rz;
 }
 
 // K1 fused: Ap_k = A p_k with gamma = p'Ap and p'p reduced in the same pass.
