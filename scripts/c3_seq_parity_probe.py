@@ -1,0 +1,36 @@
+"""The device C3 sequence against the reference's own run of it
+(tests/golden/c3_seq.npz from oracle/run_reference_c3.py): per-system
+stage-3 iterations, matvecs, q = c'x and x at 2000 fixed indices."""
+import json
+import os
+import sys
+import warnings
+
+import numpy as np
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+warnings.simplefilter("ignore")
+import paper_1512_05820_b200 as pk  # noqa: E402
+from paper_1512_05820_b200.problems import elasticity_sequence  # noqa: E402
+
+d = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests", "golden", "c3_seq.npz"))
+p = int(d["p_done"])
+seq = elasticity_sequence((64, 64, 64), p=p, rtol=1e-5, seed=3)
+cfg = pk.SolverConfig(truncation=pk.TruncationConfig(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=60,
+                                                     max_dim=60), mode="cg")
+xs, reps, _ = pk.run_sequence(seq, cfg, precond_factory=lambda A: pk.build_preconditioner("jacobi", A))
+idx = d["idx"]
+rows = []
+for j, (x, r) in enumerate(zip(xs, reps)):
+    xh = x.cpu().numpy()
+    q = float(seq.C[0] @ xh)
+    rows.append({"system": j + 1, "iters": r.stage3_iters, "ref_iters": int(d["iters"][j]),
+                 "matvecs": r.matvecs, "ref_matvecs": int(d["matvecs"][j]),
+                 "q_rel": abs(q - float(d["q"][j])) / abs(float(d["q"][j])),
+                 "x_rel": float(np.linalg.norm(xh[idx] - d["xs"][j]) / np.linalg.norm(d["xs"][j]))})
+    print(json.dumps(rows[-1]), flush=True)
+di = np.array([r["iters"] - r["ref_iters"] for r in rows])
+print(json.dumps({"systems": p, "total_iters": int(sum(r["iters"] for r in rows)),
+                  "ref_total_iters": int(d["iters"][:p].sum()), "max_abs_iter_diff": int(np.abs(di).max()),
+                  "max_q_rel": max(r["q_rel"] for r in rows), "max_x_rel": max(r["x_rel"] for r in rows),
+                  "ref_wall_s": float(d["wall"][:p].sum())}))
