@@ -778,7 +778,7 @@ def cpu_sample(host_specs, sched, cap=60, label="C3", budget_s=20.0):
     t_itm = iters_cost(Y, 8 if A.nnz < 10**8 else 4)
     t_col = max(t_itm - t_it0, 0.0) / ms
     # truncation sample: SpMM + Gram with s_cols columns, eigh at full width, S @ coef sample
-    s_cols = 32 if A.nnz < 10**8 else 8
+    s_cols = 32  # a 32 x 32 Gram sample: a narrower one understates BLAS efficiency (C4 at 8 columns: ~2x)
     Z = rng.standard_normal((n, s_cols))
     t0 = time.perf_counter()
     AZ = A @ Z

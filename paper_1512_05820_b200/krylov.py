@@ -24,13 +24,14 @@ Returned ``x`` and ``V`` are device tensors; ``vhat``, ``gamma`` and
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
 import torch
 
 from . import _native as nat
-from .errors import Breakdown, DimensionMismatch, NotConverged
+from .errors import Breakdown, DimensionMismatch, NotConverged, NotPositiveDefinite
 from .linalg import (
     F64,
     DenseLowerTriangular,
@@ -893,6 +894,27 @@ def direct_reduced_solve(A, b, W, sink: InstrumentationSink | None = None, *,
         G, AW = assemble_gram(A, Wd, sink, out=aw_out)
         g = to_numpy(G)
     g = 0.5 * (g + g.T)
-    rhat = dense_cholesky(g)
+    rhat = _cholesky(g, A.device)
     what = rhat.solve_spd(to_numpy(gemv_t(Wd, bd)))
     return DirectSolveResult(what=what, rhat=rhat, aw=AW, gram=g)
+
+
+DEVICE_CHOL_MIN = int(os.environ.get("RK_DEVICE_CHOL_MIN", "512"))
+
+
+def _cholesky(g: np.ndarray, device) -> DenseLowerTriangular:
+    """dense_cholesky (linalg.py:250-267) of the stage-1 Gram; from
+    DEVICE_CHOL_MIN columns on by cuSOLVER potrf on the device (C4: w ~ 3000,
+    seconds of host dpotrf per system), the factor kept on the device for the
+    F^{-1} the fused kernels apply and copied back for the host solves. Same
+    NotPositiveDefinite(pivot) on a failed leading minor."""
+    w = int(g.shape[0])
+    if w < DEVICE_CHOL_MIN:
+        return dense_cholesky(g)
+    Ld, info = torch.linalg.cholesky_ex(torch.from_numpy(np.ascontiguousarray(g)).to(device))
+    info = int(info)
+    if info > 0:
+        raise NotPositiveDefinite(f"leading minor of order {info} is not positive definite", pivot=info - 1)
+    rhat = DenseLowerTriangular.from_full(Ld.cpu().numpy())
+    rhat._dev[(device.type, device.index)] = as_block(Ld, device)  # linalg.DenseLowerTriangular.device cache
+    return rhat

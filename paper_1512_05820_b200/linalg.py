@@ -234,6 +234,7 @@ def hstack_blocks(blocks, n: int, device, cap_extra: int = 0) -> torch.Tensor:
 _pattern_cache_lock = threading.Lock()
 _pattern_cache: list = []  # [(host rowptr, host col, _Pattern)]
 USE_BSR3 = os.environ.get("RK_BSR", "1") != "0"
+DEVICE_SPDINV_MIN = int(os.environ.get("RK_DEVICE_SPDINV_MIN", "256"))
 USE_SELL1 = os.environ.get("RK_SELL1", "1") != "0"
 SELL1_MAX_ROW = 16      # scalar SELL for short rows (7-point stencils); longer rows keep lanes-per-row CSR
 SELL1_MAX_PAD = 1.25    # ... and only when slices pad the pattern by at most 25%
@@ -930,9 +931,17 @@ class DenseLowerTriangular:
 
     def device_spd_inverse(self, device) -> torch.Tensor:
         """Column-major device copy of F^{-1} = L^{-T} L^{-1} (host dtrtri, then a
-        w x w product): the fused kernels apply it as one symmetric mat-vec."""
+        w x w product; from DEVICE_SPDINV_MIN columns on, cuSOLVER potri on the
+        device -- at C4's w ~ 3000 the host route takes seconds per system):
+        the fused kernels apply it as one symmetric mat-vec."""
         key = ("spdinv", device.type, device.index)
         t = self._dev.get(key)
+        if t is None and self.m >= DEVICE_SPDINV_MIN:
+            L = self.device(device)  # column-major, lower
+            F = torch.cholesky_inverse(L, upper=False)
+            if not bool(torch.isfinite(F).all()):
+                raise NotPositiveDefinite("singular Cholesky factor")
+            t = self._dev[key] = as_block(F, device)
         if t is None:
             Linv, info = scipy.linalg.lapack.dtrtri(self._full, lower=1)
             if info != 0:

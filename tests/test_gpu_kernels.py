@@ -336,3 +336,18 @@ def test_scalar_sell_spmv_and_spmm(pk):
     B = pk.SparseSpdMatrix(L.n, L.row_offsets, L.col_indices, L.values, lanes=2)
     assert B.csr.bdim == 0 and B.bval is None
     np.testing.assert_allclose(pk.spmv(B, X[:, 0]).cpu().numpy(), Y[:, 0], rtol=1e-14, atol=1e-13)
+
+
+def test_device_spd_inverse_wide_factor(pk):
+    """F^{-1} of a wide dense factor (>= 256 columns) comes from cuSOLVER potri
+    on the device; it equals the host dtrtri route to rounding."""
+    import scipy.linalg
+
+    rng = np.random.default_rng(9)
+    w = 300
+    M = rng.standard_normal((w, w))
+    G = M @ M.T + w * np.eye(w)
+    L = pk.dense_cholesky(G)
+    F = L.device_spd_inverse(torch.device("cuda", 0)).cpu().numpy()
+    Li = np.tril(scipy.linalg.lapack.dtrtri(L.full(), lower=1)[0])
+    np.testing.assert_allclose(F, Li.T @ Li, rtol=1e-11, atol=1e-13 * np.abs(F).max())

@@ -180,3 +180,27 @@ def test_wide_projection_matches_oracle(pk):
     assert abs(res.k - ref.k) <= 2
     x = _np(res.x)
     assert np.linalg.norm(x - ref.x) <= 1e-8 * np.linalg.norm(ref.x)
+
+
+def test_wide_stage1_cholesky_on_device(pk):
+    """Stage-1 factors from 512 columns on come from cuSOLVER potrf: equal to
+    the host dpotrf to rounding, and an indefinite Gram raises
+    NotPositiveDefinite with the reference's pivot (first failing minor)."""
+    import torch
+
+    from paper_1512_05820_b200 import krylov
+
+    rng = np.random.default_rng(4)
+    w = 600
+    M = rng.standard_normal((w, w))
+    G = M @ M.T + w * np.eye(w)
+    dev = torch.device("cuda", 0)
+    L = krylov._cholesky(G, dev)
+    np.testing.assert_allclose(L.full(), pk.dense_cholesky(G).full(), rtol=1e-10, atol=1e-12)
+    Gbad = G.copy()
+    Gbad[300, 300] = -1.0
+    with pytest.raises(pk.NotPositiveDefinite) as e_dev:
+        krylov._cholesky(Gbad, dev)
+    with pytest.raises(pk.NotPositiveDefinite) as e_host:
+        pk.dense_cholesky(Gbad)
+    assert e_dev.value.pivot == e_host.value.pivot == 300
