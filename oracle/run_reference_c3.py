@@ -4,7 +4,11 @@ pod-a-rbf cap = max_dim = 60) and save per-system counters, q = c'x, ||x||,
 x at 2000 fixed indices and wall times to tests/golden/c3_seq.npz.
 Test infrastructure only (the GPU tests read the .npz, never the reference).
 
-python oracle/run_reference_c3.py [systems]        (CPU, ~2-3 min per system here)
+python oracle/run_reference_c3.py [systems] [perturbation]   (CPU, ~2 min per system here)
+
+With a perturbation e, every right-hand side is scaled by (1 + e) and the
+result goes to tests/golden/c3_seq_pert.npz: the reference's own rounding
+envelope on the same sequence.
 """
 import os
 import sys
@@ -19,7 +23,7 @@ sys.path.insert(0, "/root/reference/pkg/src")
 warnings.simplefilter("ignore")
 
 
-def main(p=40):
+def main(p=40, pert=0.0):
     from recykl import preconditioners
     from recykl.linalg import InstrumentationSink, SparseSpdMatrix
     from recykl.threestage import RecycleState, SolverConfig, StageTolerances, solve_system
@@ -36,10 +40,11 @@ def main(p=40):
     state = None
     for j, s in enumerate(mine, start=1):
         A = SparseSpdMatrix(s.A.n, s.A.row_offsets, s.A.col_indices, s.A.values)
+        b = s.b * (1 + pert) if pert else s.b
         if state is None:
             state = RecycleState.empty(mine.n)
         t0 = time.perf_counter()
-        x, rep, state = solve_system(A, s.b, None, state, StageTolerances(eps=s.tol), cfg,
+        x, rep, state = solve_system(A, b, None, state, StageTolerances(eps=s.tol), cfg,
                                      M=preconditioners.build("jacobi", A), sink=InstrumentationSink())
         out["wall"].append(time.perf_counter() - t0)
         out["iters"].append(rep.stage3_iters)
@@ -50,9 +55,11 @@ def main(p=40):
         d = {k: np.asarray(v) for k, v in out.items()}
         d["xs"] = np.stack(xs_s)
         d["p_done"] = np.int64(j)
-        np.savez_compressed(os.path.join(os.path.dirname(HERE), "tests", "golden", "c3_seq.npz"), **d)
+        d["perturbation"] = np.float64(pert)
+        name = "c3_seq_pert.npz" if pert else "c3_seq.npz"
+        np.savez_compressed(os.path.join(os.path.dirname(HERE), "tests", "golden", name), **d)
         print(j, rep.stage3_iters, round(out["wall"][-1], 1), flush=True)
 
 
 if __name__ == "__main__":
-    main(int(sys.argv[1]) if len(sys.argv) > 1 else 40)
+    main(int(sys.argv[1]) if len(sys.argv) > 1 else 40, float(sys.argv[2]) if len(sys.argv) > 2 else 0.0)

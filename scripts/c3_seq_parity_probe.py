@@ -13,6 +13,10 @@ warnings.simplefilter("ignore")
 import paper_1512_05820_b200 as pk  # noqa: E402
 from paper_1512_05820_b200.problems import elasticity_sequence  # noqa: E402
 
+if os.environ.get("RK_PROBE_FRESH_GRAM") == "1":  # truncation Gram by a fresh SpMM, as the reference
+    from paper_1512_05820_b200 import threestage
+
+    threestage._keep_products = lambda cfg: False
 d = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests", "golden", "c3_seq.npz"))
 p = int(d["p_done"])
 seq = elasticity_sequence((64, 64, 64), p=p, rtol=1e-5, seed=3)
