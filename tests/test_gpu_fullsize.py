@@ -122,3 +122,31 @@ def test_c3_full_size_prefix_matches_reference(pk):
     # the first system (plain Jacobi PCG) is not chaotic at the 1e-15 level: exact counters
     assert reps[0].stage3_iters == int(d["cg_stage3_iters"][0])
     assert reps[0].matvecs == int(d["cg_matvecs"][0])
+
+
+def test_c2_full_size_prefix_matches_oracle(pk):
+    """C2 at full size (128^3 diffusion, N = 2,097,152, the scalar SELL-32
+    path): its first two systems through the pinned oracle on the host and
+    through the device path give identical iteration counts and counters and
+    x / q = c'x within 1e-12 (measured: 1e-14 -- the SELL rows are scipy's
+    csr_matvec bit for bit, only the dot-product order differs)."""
+    import warnings
+
+    from oracle import recycle_oracle as O
+    from paper_1512_05820_b200.problems import diffusion3d_sequence
+
+    tr = dict(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=40, max_dim=40)
+    seq = diffusion3d_sequence(128, p=2, rtol=1e-4, seed=2)
+    specs = list(seq)
+    oxs, oreps, _ = O.run_sequence(specs, O.Config(mode="cg", **tr), precond="jacobi")
+    cfg = pk.SolverConfig(truncation=pk.TruncationConfig(**tr), mode="cg")
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        xs, reps, _ = pk.run_sequence(pk.SystemSequence(seq.n, specs, C=seq.C), cfg,
+                                      precond_factory=lambda A: pk.build_preconditioner("jacobi", A))
+    assert [r.stage3_iters for r in reps] == [r.stage3_iters for r in oreps]
+    assert [r.matvecs for r in reps] == [r.matvecs for r in oreps]
+    for x, ox in zip(xs, oxs):
+        xh = x.cpu().numpy()
+        assert np.linalg.norm(xh - ox) <= 1e-12 * np.linalg.norm(ox)
+        assert abs(seq.C[0] @ xh - seq.C[0] @ ox) <= 1e-12 * abs(seq.C[0] @ ox)
