@@ -195,3 +195,32 @@ def test_c3_sequence_within_reference_envelope(pk):
         q = float(seq.C[0] @ xh)
         assert abs(q - d["q"][j]) / abs(d["q"][j]) <= max(1e-10, 5 * env_q)
         assert np.linalg.norm(xh[idx] - d["xs"][j]) / np.linalg.norm(d["xs"][j]) <= max(1e-8, 5 * env_x)
+
+
+def test_c2_sequence_matches_reference_run(pk):
+    """The bench's C2 sequence (128^3 diffusion, 30 systems, N = 2,097,152)
+    against the reference's own run of it (tests/golden/c2_seq.npz,
+    oracle/run_reference_c2.py): the north-star bar on every system --
+    identical stage-3 iterations and counters, q = c'x within 1e-10 and x
+    (at 2000 fixed indices) within 1e-8 (measured: q <= 1e-12, x <= 6e-13)."""
+    import os
+    import warnings
+
+    from paper_1512_05820_b200.problems import diffusion3d_sequence
+
+    d = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "c2_seq.npz"))
+    p = int(d["p_done"])
+    seq = diffusion3d_sequence(128, p=p, rtol=1e-4, seed=2)
+    cfg = pk.SolverConfig(truncation=pk.TruncationConfig(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0,
+                                                         storage_cap=40, max_dim=40), mode="cg")
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        xs, reps, _ = pk.run_sequence(seq, cfg, precond_factory=lambda A: pk.build_preconditioner("jacobi", A))
+    assert [r.stage3_iters for r in reps] == d["iters"][:p].tolist()
+    assert [r.matvecs for r in reps] == d["matvecs"][:p].tolist()
+    idx = d["idx"]
+    for j, x in enumerate(xs):
+        xh = x.cpu().numpy()
+        q = float(seq.C[0] @ xh)
+        assert abs(q - d["q"][j]) <= 1e-10 * abs(d["q"][j])
+        assert np.linalg.norm(xh[idx] - d["xs"][j]) <= 1e-8 * np.linalg.norm(d["xs"][j])
