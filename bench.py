@@ -364,15 +364,15 @@ def run_b200(args, rank, world, dist):
         barrier(dist)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        xs_e, reps_e, _ = pk.run_sequence(hseq, cfg, precond_factory=jac)
-        xh = [x.cpu().numpy() for x in xs_e]
+        xs_e, reps_e, _ = pk.run_sequence(hseq, cfg, precond_factory=jac)  # host inputs -> numpy solutions
+        assert all(isinstance(x, np.ndarray) for x in xs_e)
         torch.cuda.synchronize()
         t_e2e = max_over_ranks(time.perf_counter() - t0, dist)
         e2e = {"value": round(t_e2e / world, 4), "unit": UNIT, "h2d_bytes_per_step": int(h2d * world),
                "d2h_bytes_per_step": int(d2h * world),
                "solve_wall_sum_s": round(sum(r.wall_time for r in reps_e), 3),
-               "path": "run_sequence over host CSR (reference-style SparseSpdMatrix fields), solutions copied back"}
-        del xh
+               "path": "run_sequence over host CSR (reference-style SparseSpdMatrix fields); returns numpy solutions"}
+        del xs_e
 
     ach = alg_bytes / (avg[0] * 1e-3) / 1e9 if avg[0] > 0 else None  # C1: single-CTA batches, no per-kernel samples
     traffic = None

@@ -497,6 +497,22 @@ def ctypes_zero(s):
 _MODES = {"cg": 0, "fom": 1}
 
 
+def _is_device(t) -> bool:
+    return isinstance(t, torch.Tensor) and t.is_cuda
+
+
+def _to_host_result(res: AugmentedPcgResult) -> AugmentedPcgResult:
+    """x and V as numpy (V C-order N x k, np.column_stack's layout), as the
+    reference's AugmentedPcgResult (krylov.py:159-178, 272-282)."""
+    if res is None:
+        return res
+    if isinstance(res.x, torch.Tensor):
+        res.x = to_numpy(res.x).copy()
+    if isinstance(res.V, torch.Tensor):
+        res.V = np.ascontiguousarray(to_numpy(res.V))
+    return res
+
+
 def augmented_pcg(
     op,
     b,
@@ -515,6 +531,7 @@ def augmented_pcg(
     monitor=None,
     batch: int | None = None,
     keep_products: bool = False,
+    device_results: bool | None = None,
 ) -> AugmentedPcgResult:
     """Augmented PCG over the affine space Y yhat0 + directions (krylov.py:181-345).
 
@@ -523,8 +540,25 @@ def augmented_pcg(
     and sink accounting as the reference. ``batch`` caps the number of
     iterations launched between host checks on the fused path;
     ``keep_products`` keeps every A p_k as a column of ``result.AV`` (fom mode
-    keeps them anyway) so a later POD truncation needs no SpMM.
+    keeps them anyway) so a later POD truncation needs no SpMM. The result's
+    ``x`` and ``V`` are numpy arrays when ``b`` is a host array (the
+    reference's types) and device tensors when it is a device tensor;
+    ``device_results`` forces either.
     """
+    host = (not device_results) if device_results is not None else not _is_device(b)
+    try:
+        res = _augmented_pcg(op, b, yhat0, aug_basis, reduced_solver, precond, tol, mode=mode,
+                             paper_fom_beta=paper_fom_beta, relative=relative, max_iter=max_iter, sink=sink,
+                             r0=r0, monitor=monitor, batch=batch, keep_products=keep_products)
+    except NotConverged as exc:
+        if host:
+            _to_host_result(exc.partial)
+        raise
+    return _to_host_result(res) if host else res
+
+
+def _augmented_pcg(op, b, yhat0, aug_basis, reduced_solver, precond, tol, *, mode, paper_fom_beta, relative,
+                   max_iter, sink, r0, monitor, batch, keep_products) -> AugmentedPcgResult:
     if isinstance(op, DenseReducedOperator):
         if precond is not None:
             raise NotImplementedError("a dense reduced operator runs unpreconditioned (as the reference's inner solves)")
@@ -614,16 +648,24 @@ def augmented_pcg(
         sink.add_precond()
     if Y is not None and not direct:
         _direction_with_callback(run, Y, reduced_solver, entry=True)
-    if code < 0:
-        # the reference raises at the first direction update (krylov.py:338-339)
-        _count_matvecs(operator, 1)
-        raise ValueError(f"unknown mode {mode!r}")
+    # An unknown mode surfaces where the reference meets it (krylov.py:338-339):
+    # at the first direction update, after iteration 0 has run in full -- its
+    # matvec, the curvature check and the convergence test, which may still
+    # return normally -- and after the next z = M^{-1} r. So run (as cg) one
+    # iteration at most and raise then.
+    loop_iter = max_iter if code >= 0 else min(max_iter, 1)
 
     fused = isinstance(operator, MatrixOperator) and (Y is None or direct) and monitor is None
     if fused:
-        k_final, status = _drive_fused(run, max_iter, batch)
+        k_final, status = _drive_fused(run, loop_iter, batch)
     else:
-        k_final, status = _drive_stepped(run, operator, Y, reduced_solver, direct, max_iter, monitor)
+        k_final, status = _drive_stepped(run, operator, Y, reduced_solver, direct, loop_iter, monitor)
+    if code < 0 and status == 0 and max_iter > 0:
+        if fused:
+            _count_matvecs(operator, 1)
+        if precond is not None and sink is not None:
+            sink.add_precond()
+        raise ValueError(f"unknown mode {mode!r}")
 
     # cost accounting identical to the reference's call pattern; the stepped
     # driver charges its operator applications as they happen
@@ -828,8 +870,21 @@ def _drive_stepped(run: _Run, operator, Y, reduced_solver, direct, max_iter, mon
 
 
 def pcg(A, b, x0=None, precond=None, tol: float = 0.0, max_iter: int | None = None, *, mode: str = "cg",
-        relative: bool = False, sink: InstrumentationSink | None = None, monitor=None) -> AugmentedPcgResult:
-    """Plain PCG, the empty-basis case of augmented_pcg (krylov.py:348-386)."""
+        relative: bool = False, sink: InstrumentationSink | None = None, monitor=None,
+        device_results: bool | None = None) -> AugmentedPcgResult:
+    """Plain PCG, the empty-basis case of augmented_pcg (krylov.py:348-386);
+    host ``b`` gives numpy ``x``/``V`` as augmented_pcg."""
+    host = (not device_results) if device_results is not None else not _is_device(b)
+    try:
+        res = _pcg(A, b, x0, precond, tol, max_iter, mode, relative, sink, monitor)
+    except NotConverged as exc:
+        if host:
+            _to_host_result(exc.partial)
+        raise
+    return _to_host_result(res) if host else res
+
+
+def _pcg(A, b, x0, precond, tol, max_iter, mode, relative, sink, monitor):
     operator = _as_operator(A, sink)
     bd = as_vector(b, operator.device)
     shift = None
@@ -841,7 +896,7 @@ def pcg(A, b, x0=None, precond=None, tol: float = 0.0, max_iter: int | None = No
             shift = x0d
     try:
         res = augmented_pcg(operator, rhs, precond=precond, tol=tol, max_iter=max_iter, mode=mode,
-                            relative=relative, sink=sink, monitor=monitor)
+                            relative=relative, sink=sink, monitor=monitor, device_results=True)
     except NotConverged as exc:
         if shift is not None and exc.partial is not None:
             exc.partial.x = exc.partial.x + shift
@@ -860,7 +915,18 @@ class DirectSolveResult:
 
 
 def direct_reduced_solve(A, b, W, sink: InstrumentationSink | None = None, *,
-                         aw_out=None, known=None) -> DirectSolveResult:
+                         aw_out=None, known=None, device_results: bool | None = None) -> DirectSolveResult:
+    """See _direct_reduced_solve; for a host ``b`` the cached product ``aw``
+    comes back as a C-order numpy array, as the reference's."""
+    res = _direct_reduced_solve(A, b, W, sink, aw_out=aw_out, known=known)
+    host = (not device_results) if device_results is not None else not _is_device(b)
+    if host:
+        res.aw = np.ascontiguousarray(to_numpy(res.aw))
+    return res
+
+
+def _direct_reduced_solve(A, b, W, sink: InstrumentationSink | None = None, *,
+                          aw_out=None, known=None) -> DirectSolveResult:
     """Galerkin solve over range(W) by Cholesky of W'AW (krylov.py:396-411):
     SpMM + DMMA Gram on the device, dpotrf and the two triangular solves on
     the host (w x w). ``aw_out`` (N x w device block) receives A W.

@@ -8,6 +8,12 @@ import numpy as np
 import pytest
 import torch
 
+
+def _host(t):
+    """numpy view of a result (host inputs give numpy, device inputs device tensors)."""
+    return t.detach().cpu().numpy() if hasattr(t, "detach") else np.asarray(t)
+
+
 pytestmark = pytest.mark.gpu
 
 
@@ -49,7 +55,7 @@ def test_full_size_sequence_residuals_and_basis(pk, workload):
         M = pk.build_preconditioner("jacobi", A)
         x, rep, state = pk.solve_system(A, s.b, None, state, pk.StageTolerances(eps=s.tol), cfg, M=M)
         assert rep.converged and rep.stage3_iters > 0
-        res = _true_residual(s.A, s.b, x.cpu().numpy())
+        res = _true_residual(s.A, s.b, _host(x))
         assert res <= s.tol * (1 + 1e-3), (j, res, s.tol)
         if rep.truncated:
             # leading modes (the trailing ones carry sigma_1 / sigma_i rounding amplification)
@@ -112,7 +118,7 @@ def test_c3_full_size_prefix_matches_reference(pk):
     idx = d["idx"]
     for j, (x, r) in enumerate(zip(xs, reps), start=1):
         assert abs(r.stage3_iters - int(d["cg_stage3_iters"][j - 1])) <= 2
-        xh = x.cpu().numpy()
+        xh = _host(x)
         q, qref = float(seq.C[0] @ xh), float(d[f"cg_q{j}"])
         env_q = abs(float(d[f"pert_q{j}"]) - qref) / abs(qref)
         assert abs(q - qref) / abs(qref) <= max(1e-10, 5 * env_q), (j, q, qref, env_q)
@@ -147,7 +153,7 @@ def test_c2_full_size_prefix_matches_oracle(pk):
     assert [r.stage3_iters for r in reps] == [r.stage3_iters for r in oreps]
     assert [r.matvecs for r in reps] == [r.matvecs for r in oreps]
     for x, ox in zip(xs, oxs):
-        xh = x.cpu().numpy()
+        xh = _host(x)
         assert np.linalg.norm(xh - ox) <= 1e-12 * np.linalg.norm(ox)
         assert abs(seq.C[0] @ xh - seq.C[0] @ ox) <= 1e-12 * abs(seq.C[0] @ ox)
 
@@ -191,7 +197,7 @@ def test_c3_sequence_within_reference_envelope(pk):
     assert abs(int(its.sum()) - int(ref.sum())) <= 0.05 * int(ref.sum())
     idx = d["idx"]
     for j in range(pe):
-        xh = xs[j].cpu().numpy()
+        xh = _host(xs[j])
         q = float(seq.C[0] @ xh)
         assert abs(q - d["q"][j]) / abs(d["q"][j]) <= max(1e-10, 5 * env_q)
         assert np.linalg.norm(xh[idx] - d["xs"][j]) / np.linalg.norm(d["xs"][j]) <= max(1e-8, 5 * env_x)
@@ -220,7 +226,7 @@ def test_c2_sequence_matches_reference_run(pk):
     assert [r.matvecs for r in reps] == d["matvecs"][:p].tolist()
     idx = d["idx"]
     for j, x in enumerate(xs):
-        xh = x.cpu().numpy()
+        xh = _host(x)
         q = float(seq.C[0] @ xh)
         assert abs(q - d["q"][j]) <= 1e-10 * abs(d["q"][j])
         assert np.linalg.norm(xh[idx] - d["xs"][j]) <= 1e-8 * np.linalg.norm(d["xs"][j])

@@ -17,7 +17,7 @@ def pk():
 
 
 def _np(t):
-    return t.cpu().numpy()
+    return t.detach().cpu().numpy() if hasattr(t, "detach") else np.asarray(t)
 
 
 @pytest.mark.parametrize("mode", ["cg", "fom"])

@@ -1,6 +1,8 @@
 """Whole-path parity: run_sequence on the device vs the reference's frozen
 fixtures and golden runs (counters exact, x to 1e-8, q = c'x to 1e-10)."""
 
+import json
+import os
 import warnings
 
 import numpy as np
@@ -8,6 +10,12 @@ import torch
 import pytest
 
 import golden_io as gio
+
+
+def _host(t):
+    """numpy view of a result (host inputs give numpy, device inputs device tensors)."""
+    return t.detach().cpu().numpy() if hasattr(t, "detach") else np.asarray(t)
+
 
 pytestmark = pytest.mark.gpu
 
@@ -41,7 +49,17 @@ def _sensitivity(make_seq, ocfg, c):
     return dq, dx
 
 
-def _check(d, tag, xs, reps, strict=True, c=None, sensitive=False, envelope=None):
+def _log_exact(tag, first, total):
+    """Record how many leading systems matched the reference exactly (set
+    RK_EXACT_LOG=path to collect them; the floors below come from such a run)."""
+    path = os.environ.get("RK_EXACT_LOG")
+    if path:
+        with open(path, "a") as fh:
+            fh.write(json.dumps({"case": os.environ.get("PYTEST_CURRENT_TEST", "").split(" ")[0], "tag": tag,
+                                 "exact": first, "systems": total}) + "\n")
+
+
+def _check(d, tag, xs, reps, strict=True, c=None, sensitive=False, envelope=None, min_exact=None):
     """Parity policy (BASELINE north_star): iterations within +-2 per system,
     x to 1e-8 and q = c'x to 1e-10.
 
@@ -56,8 +74,15 @@ def _check(d, tag, xs, reps, strict=True, c=None, sensitive=False, envelope=None
     want = list(map(int, cnt["stage3_iters"]))
     assert len(got) == len(want)
     first = next((j for j, (a, b) in enumerate(zip(got, want)) if a != b), len(got))
+    _log_exact(tag, first, len(got))
     if strict:
         assert first == len(got), (tag, got, want)
+    else:
+        # a non-strict case still has a floor on the systems that match exactly
+        # (counters, x to 1e-8, q to 1e-10): a change that breaks parity from
+        # system 2 on fails here, however close the later counts stay
+        assert min_exact is not None, "non-strict parity needs a floor of exactly-matched systems"
+        assert first >= min_exact, (tag, f"{first} of {len(got)} systems exact, floor {min_exact}", got, want)
     assert all(abs(a - b) <= 2 for a, b in zip(got, want)), (tag, got, want)
     exact = slice(0, first)
     for key, attr in (("matvecs", "matvecs"), ("precond_applies", "precond_applies"),
@@ -71,7 +96,7 @@ def _check(d, tag, xs, reps, strict=True, c=None, sensitive=False, envelope=None
     # every dot product, not just the input), never less than 1e-10 / 1e-8.
     base_x, base_q = (1e-6, 1e-6) if sensitive else (1e-8, 1e-10)
     for j, x in enumerate(xs, start=1):
-        xh = x.cpu().numpy()
+        xh = _host(x)
         if envelope is not None:
             base_q = max(1e-10, 50 * envelope[0][j - 1])
             base_x = max(1e-8, 50 * envelope[1][j - 1])
@@ -86,6 +111,20 @@ def _check(d, tag, xs, reps, strict=True, c=None, sensitive=False, envelope=None
             tol_q = base_q if j - 1 < first else 1e-4
             assert abs(float(c @ xh) - q_ref) <= tol_q * abs(q_ref), (tag, j)
     return first
+
+
+# Leading systems that must match the reference exactly (counters, x to 1e-8,
+# q to 1e-10) in each non-strict case: measured with RK_EXACT_LOG on a B200
+# (deterministic kernels, so the count is reproducible), never lowered.
+EXACT_FLOOR = {
+    ("stage_variants", "s2_"): 0, ("stage_variants", "s2cg_"): 0, ("stage_variants", "phi1_"): 0,
+    ("stage_variants", "prev_"): 0, ("stage_variants", "none_"): 0,
+    ("elasticity", "cg_"): 0, ("elasticity", "fom_"): 0,
+    ("c1", "fom_"): 20, ("c1", "cg_"): 20, ("c1", "s5_"): 0,
+    ("c2_small", "cg_"): 2, ("c2_small", "fom_"): 2, ("c3_mid", "cg_"): 2, ("c3_mid", "fom_"): 2,
+    ("next_strategies", "ctcr_"): 0, ("next_strategies", "ctcp_"): 0, ("next_strategies", "defl_"): 0,
+    ("next_strategies", "defs_"): 0, ("next_strategies", "ssor_"): 0, ("next_strategies", "ssor15_"): 0,
+}
 
 
 FIXTURES = {
@@ -131,7 +170,7 @@ def test_stage_variants(pk, tag):
     d = gio.load("stage_variants")
     tr, mode = STAGE[tag]
     xs, reps, _ = _run(pk, gio.sequence(d), tr, mode, "jacobi")
-    _check(d, tag, xs, reps, strict=False)
+    _check(d, tag, xs, reps, strict=False, min_exact=EXACT_FLOOR[("stage_variants", tag)])
 
 
 @pytest.mark.parametrize("tag,mode", [("cg_", "cg"), ("fom_", "fom")])
@@ -139,7 +178,7 @@ def test_elasticity_q1_sequence(pk, tag, mode):
     d = gio.load("elasticity")
     tr = dict(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=12, max_dim=12)
     xs, reps, _ = _run(pk, gio.elasticity_sequence(d), tr, mode, "jacobi")
-    _check(d, tag, xs, reps, strict=False)
+    _check(d, tag, xs, reps, strict=False, min_exact=EXACT_FLOOR[("elasticity", tag)])
 
 
 @pytest.mark.parametrize("tag,mode,extra", [("fom_", "fom", {}), ("cg_", "cg", {}), ("s5_", "fom", {"stage1_dim": 5})])
@@ -150,7 +189,8 @@ def test_c1_poisson_sequence(pk, tag, mode, extra):
     seq = poisson2d_sequence(64, p=int(d["p"]))
     tr = dict(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=20, max_dim=20, **extra)
     xs, reps, _ = _run(pk, seq, tr, mode, "jacobi")
-    first = _check(d, tag, xs, reps, strict=False, c=d["c"], sensitive=(tag == "s5_"))
+    first = _check(d, tag, xs, reps, strict=False, c=d["c"], sensitive=(tag == "s5_"),
+                   min_exact=EXACT_FLOOR[("c1", tag)])
     # the fom and cg recipes are not rounding-sensitive: all 20 systems exact
     if tag in ("fom_", "cg_"):
         assert first == len(reps)
@@ -175,7 +215,7 @@ def test_c2_c3_like_sequences(pk, name, tag, mode, cap):
     tr = dict(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=cap, max_dim=cap)
     xs, reps, _ = _run(pk, gio.pattern_sequence(d), tr, mode, "jacobi")
     env = _sensitivity(lambda: gio.pattern_sequence(d), O.Config(mode=mode, **tr), d["c"])
-    first = _check(d, tag, xs, reps, strict=False, c=d["c"], envelope=env)
+    first = _check(d, tag, xs, reps, strict=False, c=d["c"], envelope=env, min_exact=EXACT_FLOOR[(name, tag)])
     assert first >= 2  # at least the first two systems are bitwise-faithful in their counters
     if mode == "fom":  # full re-orthogonalisation is not rounding-chaotic: the plain bar holds
         assert env[0].max() < 1e-12
@@ -196,7 +236,7 @@ def test_concurrent_sequences_match_serial(pk):
         assert [r.stage3_iters for r in rep_s] == [r.stage3_iters for r in rep_c]
         assert [r.matvecs for r in rep_s] == [r.matvecs for r in rep_c]
         for a, b in zip(xs_s, xs_c):
-            assert torch.equal(a, b)  # deterministic kernels: bitwise identical
+            assert np.array_equal(a, b)  # deterministic kernels: bitwise identical
 
 
 def test_not_converged_stage3_continues_and_stops(pk):
@@ -234,7 +274,7 @@ def test_invariant_matrix_stage1_reuses_products(pk):
     assert [r.matvecs for r in rep_a] == [r.matvecs for r in rep_b]
     assert [r.stage3_iters for r in rep_a] == [r.stage3_iters for r in rep_b]
     for a, b in zip(xs_a, xs_b):
-        a, b = a.cpu().numpy(), b.cpu().numpy()
+        a, b = _host(a), _host(b)
         assert np.linalg.norm(a - b) <= 1e-10 * np.linalg.norm(b)
 
 
@@ -269,7 +309,7 @@ def test_copied_state_never_writes_into_shared_storage(pk):
         for a, b in ((specs[2], specs[3]), (specs[4], specs[5])):
             xa, _, st = pk.solve_system(A, a.b, None, st, tol, cfg, M=M)
             xb, _, other = pk.solve_system(A, b.b, None, other, tol, cfg, M=M)
-            xs += [xa.cpu().numpy(), xb.cpu().numpy()]
+            xs += [_host(xa), _host(xb)]
         return xs
 
     deep = branch_pair(False)
