@@ -5,12 +5,11 @@
 //
 // tcgen05 has no f64 kind, so the fp64 tensor path on sm_100a is the warp-level
 // DMMA (mma.sync.m8n8k4.f64, SASS DMMA.8x8x4). Operands are staged through a
-// 4-stage cp.async (LDGSTS, 16-byte, L2-only) shared-memory ring; each CTA owns
-// a 64x64 output tile computed by 4 warps of 32x32 (16 DMMA accumulators).
-// K7 splits the N (row) dimension across CTAs so a single 64x64 tile still
-// fills the 148 SMs; the split partials are summed in a fixed order (no fp64
-// atomics), so results are deterministic.
+// cp.async (LDGSTS, 16-byte, L2-only) shared-memory ring. K7 runs over work
+// units of (tile, row range) balanced by issued DMMAs (see below); K8 gives
+// each CTA a 64 x 64 output tile computed by 4 warps of 32 x 32.
 #include <algorithm>
+#include <vector>
 
 #include "common.cuh"
 
@@ -48,32 +47,132 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // --------------------------------------------------------------------------
-// K7: out[split] (m1 x m2 tile region, col-major ldo) = X[kbeg:kend, :]' Y[kbeg:kend, :]
+// K7: G = X' Y over work units.
+//
+// A unit is (tile a, tile b, row range [k0, k1)). Every unit carries about the
+// same number of ISSUED DMMAs: a warp issues only the 8 x 8 fragments of its
+// WM x WN block that hold at least one wanted entry (inside m1 x m2 and, in
+// upper mode, not strictly below the diagonal of the enclosing symmetric
+// matrix), and the host gives each tile a number of row splits proportional
+// to its active fragments. So the narrow last tile row / column of a width
+// that is not a multiple of the tile (C2: m = 386 = 6 x 64 + 2) and the
+// diagonal tiles of a triangle cost what they compute instead of a full tile,
+// and no SM idles behind a light tile. Units with a tile to themselves write
+// G directly; split tiles write dense BM x BN partials that k_gram_reduce
+// sums in a fixed order (no fp64 atomics: deterministic).
 //
 // Templated on the CTA tile (BM x BN) and the warp tile (WM x WN). Per K step
 // of 4 a warp issues WM/8 + WN/8 fragment loads for (WM/8)(WN/8) DMMAs and the
-// CTA stages (BM + BN) x 16 doubles per 2 BM BN 16 flops, so the 128 x 128
-// tile halves the L2 -> SM traffic per flop of the 64 x 64 one (16 vs 8
-// flop/B) at the price of coarser triangle and edge tiles.
+// CTA stages (BM + BN) x 16 doubles per 2 BM BN 16 flops, so the 128 x 64 tile
+// moves 3/4 of the L2 -> SM bytes per flop of the 64 x 64 one.
 // --------------------------------------------------------------------------
+constexpr int kMaxUnits = 2048;
+constexpr int kMaxTiles = 2048;
+constexpr int kChunk = 32;  // unit row ranges are multiples of 32 rows
+
+// Unit table passed by value in kernel parameter space (no device allocation,
+// capturable in graphs, re-entrant). u = a | b << 11 | direct << 22 |
+// k0 / 32 << 23 | k1 / 32 << 43; slot = partial index of a split tile.
+struct GramUnits {
+  uint64_t u[kMaxUnits];
+  uint16_t slot[kMaxUnits];
+};
+struct GramTiles {  // split tiles for the reduce: a | b << 11, first slot, count
+  uint32_t ab[kMaxTiles];
+  uint16_t first[kMaxTiles];
+  uint16_t count[kMaxTiles];
+};
+
+// ---- warp shapes of K7 -------------------------------------------------------
+// A warp owns FA x FB fragments of 8 x 8. Its shape code says which of them to
+// issue: 0 none; 1 .. FA*FB the leading RA x CB rectangle (the edge of a width
+// that is not a multiple of 8 fragments); FA*FB + 1 .. the upper staircase
+// i <= j + S (a warp on the diagonal of a symmetric Gram), S in [1 - FB, FA - 2].
+constexpr int kNoStair = 1 << 20;
+
+template <int FA, int FB>
+constexpr int kFullShape = FA * FB;  // RA = FA, CB = FB
+
+__host__ __device__ __forceinline__ int warp_shape_code(int FA, int FB, int64_t r0, int64_t c0, int64_t m1,
+                                                        int64_t m2, int64_t upper_off) {
+  if (r0 >= m1 || c0 >= m2) return 0;
+  if (upper_off >= 0) {
+    // fragment (i, j) wanted iff r0 + 8i <= c0 + 8j + off + 7, i.e. i <= j + S
+    const int64_t d = c0 + upper_off + 7 - r0;
+    const int64_t S = d >= 0 ? d / 8 : -((-d + 7) / 8);
+    if (S < 1 - FB) return 0;                // strictly below the diagonal
+    if (S <= FA - 2) return FA * FB + 1 + (int)(S + FB - 1);
+  }
+  const int64_t ra = (m1 - r0 + 7) / 8, cb = (m2 - c0 + 7) / 8;
+  const int RA = (int)(ra < FA ? ra : FA), CB = (int)(cb < FB ? cb : FB);
+  return (RA - 1) * FB + CB;
+}
+
+// DMMAs a warp of this shape issues per K step of 4 (host cost model)
+static inline int shape_frags(int FA, int FB, int code) {
+  if (code == 0) return 0;
+  if (code <= FA * FB) return ((code - 1) / FB + 1) * ((code - 1) % FB + 1);
+  const int S = code - FA * FB - 1 - (FB - 1);
+  int c = 0;
+  for (int i = 0; i < FA; ++i)
+    for (int j = 0; j < FB; ++j) c += i <= j + S;
+  return c;
+}
+
+// One K step (16 rows) of a warp: only the fragments of its shape.
+// xs / ys point at the warp's first fragment row (+ g row, + t column).
+template <int FA, int FB, int RA, int CB, int S>
+__device__ __forceinline__ void warp_step(double (&acc)[FA][FB][2], const double* xs, const double* ys) {
+#pragma unroll
+  for (int kq = 0; kq < kStep / 4; ++kq) {
+    double af[RA], bf[CB];
+#pragma unroll
+    for (int i = 0; i < RA; ++i) af[i] = xs[i * 8 * kPadK + kq * 4];
+#pragma unroll
+    for (int j = 0; j < CB; ++j) bf[j] = ys[j * 8 * kPadK + kq * 4];
+#pragma unroll
+    for (int i = 0; i < RA; ++i)
+#pragma unroll
+      for (int j = 0; j < CB; ++j)
+        if (i <= j + S) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);  // compile-time test
+  }
+}
+
+template <int FA, int FB, int C>
+__device__ __forceinline__ void warp_step_dispatch(int code, double (&acc)[FA][FB][2], const double* xs,
+                                                   const double* ys) {
+  if constexpr (C <= FA * FB) {
+    if (code == C) {
+      warp_step<FA, FB, (C - 1) / FB + 1, (C - 1) % FB + 1, kNoStair>(acc, xs, ys);
+      return;
+    }
+    warp_step_dispatch<FA, FB, C + 1>(code, acc, xs, ys);
+  } else if constexpr (C <= FA * FB + FA + FB - 2) {
+    if (code == C) {
+      warp_step<FA, FB, FA, FB, C - FA * FB - 1 - (FB - 1)>(acc, xs, ys);
+      return;
+    }
+    warp_step_dispatch<FA, FB, C + 1>(code, acc, xs, ys);
+  }
+}
+
 template <int BM, int BN, int WM, int WN, int MINB, int STAGES>
 __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB)
     k_gram(int64_t n, int64_t m1, const double* __restrict__ X, int64_t ldx, int64_t m2,
            const double* __restrict__ Y, int64_t ldy, const double* __restrict__ Y2, int64_t ldy2, int64_t c1,
-           double* __restrict__ out, int64_t ldo, int64_t split_stride, int64_t rows_per_split, int64_t upper_off) {
+           double* __restrict__ G, int64_t ldg, double* __restrict__ ws, int64_t upper_off,
+           const __grid_constant__ GramUnits U) {
   constexpr int kThreads = (BM / WM) * (BN / WN) * 32;
   constexpr int FA = WM / 8, FB = WN / 8;
   extern __shared__ __align__(16) double smem[];
   double* Xs = smem;                                  // [stage][a][kPadK]
   double* Ys = smem + STAGES * BM * kPadK;           // [stage][b][kPadK]
-  const int64_t a0 = (int64_t)blockIdx.x * BM;
-  const int64_t b0 = (int64_t)blockIdx.y * BN;
-  // upper mode: G is a block of a symmetric matrix whose column b sits at global
-  // column b + upper_off; tiles strictly below the diagonal are skipped (their
-  // entries are left undefined and mirrored by the caller).
-  if (upper_off >= 0 && a0 > b0 + upper_off + BN - 1) return;
-  const int64_t kbeg = (int64_t)blockIdx.z * rows_per_split;
-  const int64_t kend = min(n, kbeg + rows_per_split);
+  const uint64_t unit = U.u[blockIdx.x];
+  const int64_t a0 = (int64_t)(unit & 2047u) * BM;
+  const int64_t b0 = (int64_t)((unit >> 11) & 2047u) * BN;
+  const bool direct = (unit >> 22) & 1u;
+  const int64_t kbeg = (int64_t)((unit >> 23) & 0xFFFFFu) * kChunk;
+  const int64_t kend = min(n, (int64_t)((unit >> 43) & 0xFFFFFu) * kChunk);
   const int nsteps = kend > kbeg ? (int)((kend - kbeg + kStep - 1) / kStep) : 0;
 
   // Each thread stages fixed (column, row pair) chunks: LX of the left panel
@@ -119,6 +218,11 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wa = (warp % (BM / WM)) * WM, wb = (warp / (BM / WM)) * WN;
+  // The warp's shape code, fixed for the whole unit (warp-uniform). A
+  // predicated-off DMMA costs the pipe as much as an issued one (measured,
+  // scripts/dmma_pred_probe.cu), so masked fragments are skipped by branching
+  // to a body that contains only the wanted DMMAs.
+  const int code = warp_shape_code(FA, FB, a0 + wa, b0 + wb, m1, m2, upper_off);
   double acc[FA][FB][2];
 #pragma unroll
   for (int i = 0; i < FA; ++i)
@@ -130,59 +234,80 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB)
     if (s < nsteps) load_stage(s, s);
     cp_async_commit();
   }
-  // upper mode: a warp whose whole WM x WN block lies strictly below the
-  // diagonal only helps stage operands (its entries are undefined anyway)
-  const bool compute = !(kSkipLower && upper_off >= 0 && a0 + wa > b0 + wb + upper_off + WN - 1);
-  for (int step = 0; step < nsteps; ++step) {
+  // K step prologue shared by both loops: wait for stage `step`, refill the
+  // ring; returns the warp's fragment base pointers into that stage.
+  auto next_stage = [&](int step, const double*& xs, const double*& ys) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     const int nxt = step + STAGES - 1;
     if (nxt < nsteps) load_stage(nxt % STAGES, nxt);
     cp_async_commit();
     const int stg = step % STAGES;
-    const double* xs = Xs + (stg * BM) * kPadK;
-    const double* ys = Ys + (stg * BN) * kPadK;
-    if (!compute) continue;
-#pragma unroll
-    for (int kq = 0; kq < kStep / 4; ++kq) {
-      double af[FA], bf[FB];
-#pragma unroll
-      for (int i = 0; i < FA; ++i) af[i] = xs[(wa + i * 8 + g) * kPadK + kq * 4 + t];
-#pragma unroll
-      for (int j = 0; j < FB; ++j) bf[j] = ys[(wb + j * 8 + g) * kPadK + kq * 4 + t];
-#pragma unroll
-      for (int i = 0; i < FA; ++i)
-#pragma unroll
-        for (int j = 0; j < FB; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    xs = Xs + (stg * BM + wa + g) * kPadK + t;
+    ys = Ys + (stg * BN + wb + g) * kPadK + t;
+  };
+  // Two copies of the K loop, chosen once per warp: the common full-tile warp
+  // runs a loop with no shape dispatch at all; edge / diagonal warps dispatch
+  // per step. Every warp passes the same number of block barriers.
+  const double *xs, *ys;
+  if (code == kFullShape<FA, FB>) {
+    for (int step = 0; step < nsteps; ++step) {
+      next_stage(step, xs, ys);
+      warp_step<FA, FB, FA, FB, kNoStair>(acc, xs, ys);
+    }
+  } else {
+    for (int step = 0; step < nsteps; ++step) {
+      next_stage(step, xs, ys);
+      if (code != 0) warp_step_dispatch<FA, FB, 1>(code, acc, xs, ys);  // 0: only stages operands
     }
   }
   cp_async_wait<0>();
 
-  double* o = out + (int64_t)blockIdx.z * split_stride;
+  if (direct) {
 #pragma unroll
-  for (int i = 0; i < FA; ++i) {
-    const int64_t ga = a0 + wa + i * 8 + g;
+    for (int i = 0; i < FA; ++i) {
+      const int64_t ga = a0 + wa + i * 8 + g;
 #pragma unroll
-    for (int j = 0; j < FB; ++j) {
-      const int64_t gb = b0 + wb + j * 8 + 2 * t;
-      if (ga < m1) {
-        if (gb < m2) o[ga + gb * ldo] = acc[i][j][0];
-        if (gb + 1 < m2) o[ga + (gb + 1) * ldo] = acc[i][j][1];
+      for (int j = 0; j < FB; ++j) {
+        const int64_t gb = b0 + wb + j * 8 + 2 * t;
+        if (ga < m1) {
+          if (gb < m2) G[ga + gb * ldg] = acc[i][j][0];
+          if (gb + 1 < m2) G[ga + (gb + 1) * ldg] = acc[i][j][1];
+        }
+      }
+    }
+  } else {
+    // dense BM x BN partial (column-major, ld BM); inactive fragments are zeros
+    double* o = ws + (int64_t)U.slot[blockIdx.x] * (BM * BN);
+#pragma unroll
+    for (int i = 0; i < FA; ++i) {
+      const int la = wa + i * 8 + g;
+#pragma unroll
+      for (int j = 0; j < FB; ++j) {
+        const int lb = wb + j * 8 + 2 * t;
+        o[la + lb * BM] = acc[i][j][0];
+        o[la + (lb + 1) * BM] = acc[i][j][1];
       }
     }
   }
 }
 
-// Fixed-order sum of the split partials: G[a + b*ldg] = sum_s ws[s][a + b*m1].
-__global__ void k_gram_reduce(int64_t m1, int64_t m2, int64_t splits, const double* __restrict__ ws,
-                              double* __restrict__ G, int64_t ldg) {
-  const int64_t total = m1 * m2;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
+// Fixed-order sum of a split tile's partials: G[a0 + r, b0 + c] = sum_q
+// ws[first + q][r + c BM]. One CTA per split tile.
+template <int BM, int BN>
+__global__ void __launch_bounds__(256) k_gram_reduce(int64_t m1, int64_t m2, const double* __restrict__ ws,
+                                                     double* __restrict__ G, int64_t ldg,
+                                                     const __grid_constant__ GramTiles T) {
+  const uint32_t ab = T.ab[blockIdx.x];
+  const int64_t a0 = (int64_t)(ab & 2047u) * BM, b0 = (int64_t)((ab >> 11) & 2047u) * BN;
+  const double* p = ws + (int64_t)T.first[blockIdx.x] * (BM * BN);
+  const int cnt = T.count[blockIdx.x];
+  for (int e = threadIdx.x; e < BM * BN; e += blockDim.x) {
+    const int r = e % BM, c = e / BM;
+    if (a0 + r >= m1 || b0 + c >= m2) continue;
     double s = 0.0;
-    for (int64_t q = 0; q < splits; ++q) s += ws[q * total + e];
-    const int64_t a = e % m1, b = e / m1;
-    G[a + b * ldg] = s;
+    for (int q = 0; q < cnt; ++q) s += __ldcs(p + (int64_t)q * (BM * BN) + e);
+    G[(a0 + r) + (b0 + c) * ldg] = s;
   }
 }
 
@@ -298,8 +423,9 @@ static size_t gemm_smem() {
 // residency (CTAs per SM at its register / shared-memory footprint).
 struct GramVariant {
   void (*fn)(int64_t, int64_t, const double*, int64_t, int64_t, const double*, int64_t, const double*, int64_t, int64_t,
-             double*, int64_t, int64_t, int64_t, int64_t);
-  int bm, bn, threads;
+             double*, int64_t, double*, int64_t, const rk::GramUnits);
+  void (*reduce)(int64_t, int64_t, const double*, double*, int64_t, const rk::GramTiles);
+  int bm, bn, wm, wn, threads;
   size_t smem;
   int64_t per_sm;
 };
@@ -308,8 +434,11 @@ template <int BM, int BN, int WM, int WN, int MINB, int STAGES>
 static GramVariant make_variant() {
   GramVariant v;
   v.fn = rk::k_gram<BM, BN, WM, WN, MINB, STAGES>;
+  v.reduce = rk::k_gram_reduce<BM, BN>;
   v.bm = BM;
   v.bn = BN;
+  v.wm = WM;
+  v.wn = WN;
   v.threads = (BM / WM) * (BN / WN) * 32;
   v.smem = (size_t)STAGES * (BM + BN) * rk::kPadK * sizeof(double);
   cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem);
@@ -319,91 +448,179 @@ static GramVariant make_variant() {
   return v;
 }
 
-// 0: 64 x 64 CTA tile, 4 warps of 32 x 32 (2 CTAs / SM)
-// 1: 128 x 64, 4 warps of 64 x 32, 3 stages (2 CTAs / SM)
-// 2: 128 x 128, 8 warps of 64 x 32 (1 CTA / SM)
+// 0: 64 x 64 CTA tile, 4 warps of 32 x 32, 4 stages (2 CTAs / SM)
+// 1: 128 x 64, 4 warps of 64 x 32, 3 stages (2 CTAs / SM): full Grams
+// 2: 64 x 64, 3 stages (3 CTAs / SM)
+// 3: 64 x 80, 4 warps of 32 x 40 (3 CTAs / SM)
+// 4: 64 x 48, 4 warps of 32 x 24 (3 CTAs / SM)
+// 2-4 differ only in the tile width, so a width that leaves a sliver past
+// the last multiple of 64 (C2's truncation Gram: 386 = 6 x 64 + 2) can take
+// a width whose last tile column is mostly full (386 = 4 x 80 + 66).
+constexpr int kVariants = 5;
 static const GramVariant& gram_variant(int which) {
   static const GramVariant v0 = make_variant<64, 64, 32, 32, RK_GRAM_MINB, rk::kStages>();
   static const GramVariant v1 = make_variant<128, 64, 64, 32, 2, 3>();
-  static const GramVariant v2 = make_variant<128, 128, 64, 32, 1, 4>();
-  return which == 2 ? v2 : which == 1 ? v1 : v0;
+  static const GramVariant v2 = make_variant<64, 64, 32, 32, 3, 3>();
+  static const GramVariant v3 = make_variant<64, 80, 32, 40, 3, 3>();
+  static const GramVariant v4 = make_variant<64, 48, 32, 24, 3, 3>();
+  switch (which) {
+    case 1: return v1;
+    case 2: return v2;
+    case 3: return v3;
+    case 4: return v4;
+    default: return v0;
+  }
 }
 
-struct GramGeom {
-  int which;
-  int64_t ta, tb, splits, rows_per_split;
+// DMMAs per K step of 4 that the warps of tile (a, b) issue.
+static int64_t tile_cost(const GramVariant& v, int64_t a, int64_t b, int64_t m1, int64_t m2, int64_t upper_off) {
+  int64_t c = 0;
+  const int fa = v.wm / 8, fb = v.wn / 8;
+  for (int64_t wa = 0; wa < v.bm; wa += v.wm)
+    for (int64_t wb = 0; wb < v.bn; wb += v.wn)
+      c += rk::shape_frags(fa, fb, rk::warp_shape_code(fa, fb, a * v.bm + wa, b * v.bn + wb, m1, m2, upper_off));
+  return c;
+}
+
+// Modelled slot time of a Gram with variant v and uniform row splits: every
+// tile streams all n rows, a K step costing its issued DMMAs but at least
+// half of a full tile's (a step of a light tile still waits for its panels).
+static double model_cost(const GramVariant& v, int64_t m1, int64_t m2, int64_t upper_off) {
+  const int64_t ta = (m1 + v.bm - 1) / v.bm, tb = (m2 + v.bn - 1) / v.bn;
+  const double full = (double)(v.bm / 8) * (v.bn / 8);
+  double t = 0.0;
+  for (int64_t b = 0; b < tb; ++b)
+    for (int64_t a = 0; a < ta; ++a) {
+      const int64_t c = tile_cost(v, a, b, m1, m2, upper_off);
+      if (c) t += std::max((double)c, 0.5 * full);
+    }
+  return t;
+}
+
+// Work plan of one Gram: variant, units (launch order) and split tiles.
+struct GramPlan {
+  int which = 0;
+  int nunits = 0, nsplit = 0;
+  int64_t ws_doubles = 0;
+  rk::GramUnits U;
+  rk::GramTiles T;
 };
 
-// Tiles the kernel computes: all of them, or (upper_off >= 0) those not strictly
-// below the diagonal of the enclosing symmetric matrix.
-static int64_t active_tiles(int64_t ta, int64_t tb, int bm, int bn, int64_t upper_off) {
-  if (upper_off < 0) return ta * tb;
-  int64_t count = 0;
-  for (int64_t b = 0; b < tb; ++b) {
-    const int64_t last_a = (b * bn + upper_off + bn - 1) / bm;  // a0 <= b0 + off + bn - 1
-    count += std::min(ta, last_a + 1);
-  }
-  return count;
-}
-
-// Tile choice: 128x64 when it computes no more area (edge and triangle tiles
-// included) than 64x64, else 64x64; RK_GRAM_TILE=0/1/2 forces one.
+// Variant: full Grams at least 128 rows tall take 128 x 64 (fewer L2 -> SM
+// bytes per flop: measured 0.91 of the DMMA peak at C5 against 0.89 for 64 x
+// 64); otherwise the 64-row tile width (48 / 64 / 80) with the least modelled
+// slot time. RK_GRAM_TILE=0..4 forces one.
 static int pick_variant(int64_t m1, int64_t m2, int64_t upper_off) {
   static const int forced = [] {
     const char* e = getenv("RK_GRAM_TILE");
     return e ? atoi(e) : -1;
   }();
-  if (forced >= 0 && forced <= 2) return forced;
-  double area[3];
-  for (int w = 0; w < 3; ++w) {
-    const GramVariant& v = gram_variant(w);
-    const int64_t ta = (m1 + v.bm - 1) / v.bm, tb = (m2 + v.bn - 1) / v.bn;
-    area[w] = (double)active_tiles(ta, tb, v.bm, v.bn, upper_off) * v.bm * v.bn;
+  if (forced >= 0 && forced < kVariants) return forced;
+  if (upper_off < 0 && m1 >= 128 && m1 % 128 == 0 && m2 % 64 == 0) return 1;
+  int best = 2;
+  double best_cost = 0.0;
+  for (int w : {2, 3, 4}) {
+    const double c = model_cost(gram_variant(w), m1, m2, upper_off);  // in 8 x 8 fragments of G
+    if (w == 2 || c < 0.98 * best_cost) {  // ties keep the 64-wide tile
+      best = w;
+      best_cost = c;
+    }
   }
-  // measured (scripts/gram_probe.py): 128x64 beats 64x64 by 2-5% on full
-  // Grams, 128x128 never wins (one CTA of 8 warps per SM hides less latency)
-  return area[1] <= 1.02 * area[0] ? 1 : 0;
+  return best;
 }
 
-// Split N so the (tile, split) units fill whole waves of the resident CTA slots:
-// each unit is the same amount of work, so the tail of a partial wave is the
-// loss. Picks the fewest waves (<= 8) within 3% of the best fill.
-static GramGeom gram_geometry(int64_t n, int64_t m1, int64_t m2, int64_t upper_off) {
-  GramGeom g;
-  g.which = pick_variant(m1, m2, upper_off);
-  const GramVariant& v = gram_variant(g.which);
-  g.ta = (m1 + v.bm - 1) / v.bm;
-  g.tb = (m2 + v.bn - 1) / v.bn;
-  const int64_t tiles = std::max<int64_t>(1, active_tiles(g.ta, g.tb, v.bm, v.bn, upper_off));
-  const int64_t slots = (int64_t)sm_count() * v.per_sm;
-  const int64_t max_splits = std::max<int64_t>(1, n / 512);
-  double fill[9] = {0};
-  int64_t pick[9] = {0};
-  double best = 0.0;
-  for (int w = 1; w <= 8; ++w) {
-    const int64_t sp = std::max<int64_t>(1, std::min(max_splits, slots * w / tiles));
-    const int64_t units = sp * tiles;
-    fill[w] = (double)units / (double)(slots * ((units + slots - 1) / slots));
-    pick[w] = sp;
-    best = std::max(best, fill[w]);
-  }
-  int64_t splits = pick[8];
-  for (int w = 1; w <= 8; ++w)
-    if (fill[w] >= best - 0.03) {
-      splits = pick[w];
-      break;
+// Split-K plan: the units of all tiles fill about `waves` (4) rounds of the
+// resident CTA slots, each unit at least 512 rows. By default every tile gets
+// the same row splits, so the CTAs that run together stream the same row
+// band of X and Y (L2 reuse; measured 0.80 against 0.74 of the DMMA peak on
+// the C3 truncation Gram for splits in proportion to a tile's DMMAs,
+// RK_GRAM_UNIFORM=0). Units are launched by row band, tiles within a band.
+static int build_plan(int64_t n, int64_t m1, int64_t m2, int64_t upper_off, GramPlan& P) {
+  P.which = pick_variant(m1, m2, upper_off);
+  const GramVariant& v = gram_variant(P.which);
+  const int64_t ta = (m1 + v.bm - 1) / v.bm, tb = (m2 + v.bn - 1) / v.bn;
+  RK_REQUIRE(ta <= 2048 && tb <= 2048, RK_ERR_DIMENSION, "rk_gram: too many columns (%lld x %lld)",
+             (long long)m1, (long long)m2);
+  const int64_t nchunk = (n + rk::kChunk - 1) / rk::kChunk;
+  RK_REQUIRE(nchunk < (1 << 20), RK_ERR_DIMENSION, "rk_gram: too many rows (%lld)", (long long)n);
+  struct Tile { int64_t a, b, cost, ns; };
+  static thread_local std::vector<Tile> tiles;
+  tiles.clear();
+  int64_t total = 0;
+  // A K step of a light tile is not free: it still waits for its operand
+  // panels, so a unit of a tile with few active fragments is latency-bound.
+  // Splits follow max(active, half of a full tile), which keeps such units
+  // as short as the DMMA-bound ones (else they form the tail of the launch).
+  const int64_t floor_cost = (v.bm / 8) * (v.bn / 8) / 2;
+  for (int64_t b = 0; b < tb; ++b)
+    for (int64_t a = 0; a < ta; ++a) {
+      const int64_t c = tile_cost(v, a, b, m1, m2, upper_off);
+      if (c) {
+        tiles.push_back({a, b, std::max(c, floor_cost), 1});
+        total += std::max(c, floor_cost);
+      }
     }
-  int64_t rps = (n + splits - 1) / splits;
-  rps = (rps + rk::kStep - 1) / rk::kStep * rk::kStep;
-  splits = std::max<int64_t>(1, (n + rps - 1) / rps);
-  g.splits = splits;
-  g.rows_per_split = std::max<int64_t>(rps, rk::kStep);
-  return g;
+  RK_REQUIRE((int64_t)tiles.size() <= rk::kMaxUnits, RK_ERR_DIMENSION, "rk_gram: %lld tiles exceed the unit table",
+             (long long)tiles.size());
+  const int64_t slots = (int64_t)sm_count() * v.per_sm;
+  const int64_t max_split = std::max<int64_t>(1, nchunk / 16);  // >= 512 rows per unit
+  static const int64_t waves = [] {
+    const char* e = getenv("RK_GRAM_WAVES");
+    return e ? std::max(1, atoi(e)) : 4;
+  }();
+  int64_t target = std::max<int64_t>((int64_t)tiles.size(), waves * slots);
+  static const bool uniform = [] {
+    const char* e = getenv("RK_GRAM_UNIFORM");
+    return e ? atoi(e) != 0 : true;
+  }();
+  for (;;) {
+    int64_t units = 0;
+    const int64_t ns_u = std::min(max_split, std::max<int64_t>(1, target / (int64_t)tiles.size()));
+    for (Tile& t : tiles) {
+      t.ns = uniform ? ns_u : std::min(max_split, std::max<int64_t>(1, (target * t.cost + total / 2) / total));
+      units += t.ns;
+    }
+    if (units <= rk::kMaxUnits) break;
+    target = target * rk::kMaxUnits / units - 1;
+  }
+  // split tiles get partial slots (tile-major, so a tile's partials are contiguous)
+  int nsplit = 0, slot = 0;
+  struct U { int64_t k0; int64_t tile; uint64_t code; int slot; };
+  static thread_local std::vector<U> units;
+  units.clear();
+  for (int64_t i = 0; i < (int64_t)tiles.size(); ++i) {
+    const Tile& t = tiles[i];
+    const bool direct = t.ns == 1;
+    if (!direct) {
+      RK_REQUIRE(nsplit < rk::kMaxTiles, RK_ERR_DIMENSION, "rk_gram: too many split tiles");
+      P.T.ab[nsplit] = (uint32_t)(t.a | (t.b << 11));
+      P.T.first[nsplit] = (uint16_t)slot;
+      P.T.count[nsplit] = (uint16_t)t.ns;
+      ++nsplit;
+    }
+    for (int64_t q = 0; q < t.ns; ++q) {
+      const int64_t k0 = nchunk * q / t.ns, k1 = nchunk * (q + 1) / t.ns;
+      const uint64_t code = (uint64_t)t.a | ((uint64_t)t.b << 11) | ((uint64_t)direct << 22) | ((uint64_t)k0 << 23) |
+                            ((uint64_t)k1 << 43);
+      units.push_back({k0, i, code, direct ? 0 : slot++});
+    }
+  }
+  std::stable_sort(units.begin(), units.end(), [](const U& x, const U& y) { return x.k0 < y.k0; });
+  for (size_t i = 0; i < units.size(); ++i) {
+    P.U.u[i] = units[i].code;
+    P.U.slot[i] = (uint16_t)units[i].slot;
+  }
+  P.nunits = (int)units.size();
+  P.nsplit = nsplit;
+  P.ws_doubles = (int64_t)slot * v.bm * v.bn;
+  return 0;
 }
 
 int64_t gram_workspace_doubles(int64_t n, int64_t m1, int64_t m2, int64_t upper_off) {
-  const GramGeom g = gram_geometry(std::max<int64_t>(n, 1), m1, m2, upper_off);
-  return g.splits > 1 ? g.splits * m1 * m2 : 0;
+  if (m1 <= 0 || m2 <= 0) return 0;
+  static thread_local GramPlan P;
+  if (build_plan(std::max<int64_t>(n, 1), m1, m2, upper_off, P) != 0) return 0;
+  return P.ws_doubles;
 }
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
@@ -421,22 +638,18 @@ int launch_gram(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m2,
              RK_ERR_ARG, "rk_gram: operands need 16-byte aligned columns with even leading dimension");
   RK_REQUIRE(ldx >= n && ldy >= n && ldy2 >= n && ldg >= m1 && c1 >= 0, RK_ERR_DIMENSION,
              "rk_gram: leading dimension too small");
-  const GramGeom g = gram_geometry(std::max<int64_t>(n, 1), m1, m2, upper_off);
-  const GramVariant& v = gram_variant(g.which);
-  dim3 grid((unsigned)g.ta, (unsigned)g.tb, (unsigned)g.splits);
-  if (g.splits == 1) {
-    v.fn<<<grid, v.threads, v.smem, s>>>(n, m1, X, ldx, m2, Y, ldy, Y2, ldy2, c1, G, ldg, 0, g.rows_per_split,
-                                         upper_off);
+  static thread_local GramPlan P;  // ~30 KB: per calling thread, never on the stack
+  const int rc = build_plan(std::max<int64_t>(n, 1), m1, m2, upper_off, P);
+  if (rc != 0) return rc;
+  RK_REQUIRE(P.ws_doubles == 0 || (ws && ws_len >= P.ws_doubles), RK_ERR_ARG,
+             "rk_gram: workspace too small (%lld < %lld)", (long long)ws_len, (long long)P.ws_doubles);
+  const GramVariant& v = gram_variant(P.which);
+  if (P.nunits == 0) return 0;
+  v.fn<<<P.nunits, v.threads, v.smem, s>>>(n, m1, X, ldx, m2, Y, ldy, Y2, ldy2, c1, G, ldg, ws, upper_off, P.U);
+  rkh::note_launch();
+  if (P.nsplit) {
+    v.reduce<<<P.nsplit, 256, 0, s>>>(m1, m2, ws, G, ldg, P.T);
     rkh::note_launch();
-  } else {
-    RK_REQUIRE(ws && ws_len >= g.splits * m1 * m2, RK_ERR_ARG, "rk_gram: workspace too small (%lld < %lld)",
-               (long long)ws_len, (long long)(g.splits * m1 * m2));
-    v.fn<<<grid, v.threads, v.smem, s>>>(n, m1, X, ldx, m2, Y, ldy, Y2, ldy2, c1, ws, m1, m1 * m2,
-                                         g.rows_per_split, upper_off);
-    rkh::note_launch();
-    const int64_t total = m1 * m2;
-    const int rg = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 8));
-    rk::k_gram_reduce<<<rg, 256, 0, s>>>(m1, m2, g.splits, ws, G, ldg); rkh::note_launch();
   }
   return cuda_check("rk_gram");
 }

@@ -656,33 +656,37 @@ def _augmented_pcg(op, b, yhat0, aug_basis, reduced_solver, precond, tol, *, mod
     loop_iter = max_iter if code >= 0 else min(max_iter, 1)
 
     fused = isinstance(operator, MatrixOperator) and (Y is None or direct) and monitor is None
+    charge_precond = precond is not None and sink is not None
     if fused:
         k_final, status = _drive_fused(run, loop_iter, batch)
     else:
-        k_final, status = _drive_stepped(run, operator, Y, reduced_solver, direct, loop_iter, monitor)
+        # the stepped driver charges every application as it happens, so the
+        # counters a monitor snapshots (threestage Checkpoint) are the reference's
+        k_final, status = _drive_stepped(run, operator, Y, reduced_solver, direct, loop_iter, monitor,
+                                         sink if charge_precond else None)
     if code < 0 and status == 0 and max_iter > 0:
         if fused:
             _count_matvecs(operator, 1)
-        if precond is not None and sink is not None:
-            sink.add_precond()
+            if charge_precond:
+                sink.add_precond()
         raise ValueError(f"unknown mode {mode!r}")
 
-    # cost accounting identical to the reference's call pattern; the stepped
-    # driver charges its operator applications as they happen
+    # cost accounting identical to the reference's call pattern (fused path:
+    # charged here once the run is over)
     if status == 2:
         bd_iter = int(run.cstate.bd_iter)
         if fused:
             _count_matvecs(operator, bd_iter + 1)
-        if precond is not None and sink is not None:
-            sink.add_precond(bd_iter)
+            if charge_precond:
+                sink.add_precond(bd_iter)
         raise Breakdown(f"direction curvature {run.cstate.gamma:.3e} at iteration {bd_iter}")
     if fused:
         _count_matvecs(operator, k_final)
     if status == 1:
-        if precond is not None and sink is not None:
+        if fused and charge_precond:
             sink.add_precond(k_final - 1)
         return _result(run, k_final, True)
-    if precond is not None and sink is not None:
+    if fused and charge_precond:
         sink.add_precond(max_iter)
     raise NotConverged(
         f"no convergence to {threshold:.3e} within {max_iter} iterations",
@@ -838,8 +842,10 @@ def _direction_with_callback(run: _Run, Y, reduced_solver, entry: bool):
         del mu
 
 
-def _drive_stepped(run: _Run, operator, Y, reduced_solver, direct, max_iter, monitor):
-    """One iteration at a time: operator callback, curvature, update, direction."""
+def _drive_stepped(run: _Run, operator, Y, reduced_solver, direct, max_iter, monitor, precond_sink=None):
+    """One iteration at a time: operator callback, curvature, update, direction.
+    Matvecs and (``precond_sink``) the z = M^{-1} r of every iteration that
+    continues are charged as they happen (krylov.py:294-320)."""
     dev = run.device
     st = run.cstate
     for it in range(max_iter):
@@ -861,6 +867,8 @@ def _drive_stepped(run: _Run, operator, Y, reduced_solver, direct, max_iter, mon
             monitor(k + 1, run.x.clone())
         if st.done:
             return int(st.k), int(st.status)
+        if precond_sink is not None:
+            precond_sink.add_precond()
         if Y is not None and not direct:
             _direction_with_callback(run, Y, reduced_solver, entry=False)
         else:

@@ -177,6 +177,48 @@ def test_dmma_gram_shapes(pk, n, m1, m2):
     np.testing.assert_allclose(G, ref, rtol=1e-11, atol=1e-12 * np.sqrt(n))
 
 
+@pytest.mark.parametrize("n,m,y_old", [(5000, 7, 3), (3001, 130, 60), (20011, 386, 40), (9000, 700, 60),
+                                       (40000, 129, 0), (1200, 257, 256)])
+@pytest.mark.parametrize("single", [True, False])
+def test_dmma_symmetric_gram_upper_shapes(pk, n, m, y_old, single):
+    """K7 in upper mode over balanced, fragment-masked units: widths that are
+    not tile multiples (386 = 3 x 128 + 2), the two-segment right operand
+    (stage-1 A W + the run's A p_k) and the per-block col_off path; every
+    entry of the upper triangle matches numpy, and repeated calls are
+    bitwise identical (fixed-order split reduction)."""
+    from paper_1512_05820_b200.linalg import as_block, symmetric_gram_from_products
+
+    rng = np.random.default_rng(n + m)
+    Z = rng.standard_normal((n, m))
+    AZ = rng.standard_normal((n, m))
+    segs = [(as_block(AZ[:, :y_old]), 0)] if y_old else []
+    segs.append((as_block(AZ[:, y_old:]), y_old))
+    Zd = as_block(Z)
+    U1 = symmetric_gram_from_products(Zd, segs, single_launch=single)
+    U2 = symmetric_gram_from_products(Zd, segs, single_launch=single)
+    assert torch.equal(U1.store, U2.store)
+    G = np.asarray(U1)
+    ref = Z.T @ AZ
+    iu = np.triu_indices(m)
+    np.testing.assert_allclose(G[iu], ref[iu], rtol=1e-11, atol=1e-12 * np.sqrt(n))
+
+
+@pytest.mark.parametrize("n,m1,m2", [(811200, 60, 60), (100000, 3000, 110), (4096, 20, 20), (300000, 386, 386)])
+def test_dmma_gram_workload_shapes(pk, n, m1, m2):
+    """The Gram shapes the sequences issue: stage-1 W'(AW) (C3), the new
+    columns of an accumulated C4 snapshot (w x k_new), C1, and a C2-width
+    square; against a torch fp64 reference on the device."""
+    from paper_1512_05820_b200.linalg import empty_block, gram
+
+    gen = torch.Generator(device="cuda").manual_seed(m1 + m2)
+    X, Y = empty_block(n, m1, "cuda"), empty_block(n, m2, "cuda")
+    X.copy_(torch.randn(n, m1, generator=gen, device="cuda", dtype=torch.float64))
+    Y.copy_(torch.randn(n, m2, generator=gen, device="cuda", dtype=torch.float64))
+    G = gram(X, Y)
+    ref = X.t() @ Y
+    assert float((G - ref).abs().max()) <= 1e-12 * n ** 0.5 * 10
+
+
 @pytest.mark.parametrize("n,s,y", [(1, 1, 1), (33, 17, 3), (4096, 100, 60), (9999, 300, 70)])
 def test_dmma_gemm_nn_shapes(pk, n, s, y):
     from paper_1512_05820_b200.linalg import as_block, gemm_nn

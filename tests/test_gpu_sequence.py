@@ -115,15 +115,17 @@ def _check(d, tag, xs, reps, strict=True, c=None, sensitive=False, envelope=None
 
 # Leading systems that must match the reference exactly (counters, x to 1e-8,
 # q to 1e-10) in each non-strict case: measured with RK_EXACT_LOG on a B200
-# (deterministic kernels, so the count is reproducible), never lowered.
+# (deterministic kernels, so the count is reproducible; profiles/r02/
+# exact_matches.jsonl), never lowered. Every case currently matches on every
+# system, so each floor is the case's full length.
 EXACT_FLOOR = {
-    ("stage_variants", "s2_"): 0, ("stage_variants", "s2cg_"): 0, ("stage_variants", "phi1_"): 0,
-    ("stage_variants", "prev_"): 0, ("stage_variants", "none_"): 0,
-    ("elasticity", "cg_"): 0, ("elasticity", "fom_"): 0,
-    ("c1", "fom_"): 20, ("c1", "cg_"): 20, ("c1", "s5_"): 0,
-    ("c2_small", "cg_"): 2, ("c2_small", "fom_"): 2, ("c3_mid", "cg_"): 2, ("c3_mid", "fom_"): 2,
-    ("next_strategies", "ctcr_"): 0, ("next_strategies", "ctcp_"): 0, ("next_strategies", "defl_"): 0,
-    ("next_strategies", "defs_"): 0, ("next_strategies", "ssor_"): 0, ("next_strategies", "ssor15_"): 0,
+    ("stage_variants", "s2_"): 5, ("stage_variants", "s2cg_"): 5, ("stage_variants", "phi1_"): 5,
+    ("stage_variants", "prev_"): 5, ("stage_variants", "none_"): 5,
+    ("elasticity", "cg_"): 4, ("elasticity", "fom_"): 4,
+    ("c1", "fom_"): 20, ("c1", "cg_"): 20, ("c1", "s5_"): 20,
+    ("c2_small", "cg_"): 4, ("c2_small", "fom_"): 4, ("c3_mid", "cg_"): 3, ("c3_mid", "fom_"): 3,
+    ("next_strategies", "ctcr_"): 6, ("next_strategies", "ctcp_"): 6, ("next_strategies", "defl_"): 6,
+    ("next_strategies", "defs_"): 6, ("next_strategies", "ssor_"): 6, ("next_strategies", "ssor15_"): 6,
 }
 
 
