@@ -3,11 +3,15 @@
 // One iteration k is three kernels (plus four for the fom re-orthogonalisation):
 //   k_spmv_pcg  (spmv.cu)  Ap_k = A p_k, gamma, p'p, breakdown test, alpha
 //   k_pcg_update           x += alpha p_k, r -= alpha Ap_k, z = D^{-1} r, ||r||^2, r'z,
-//                          c = cross' z; the last block to finish combines the
-//                          block partials in a fixed order, records ||r||, decides
-//                          convergence, and solves mu = F^{-1} c
-//   k_pcg_direction        p_{k+1} = z + beta p_k - B mu (cg) | z - B mu (fom),
+//                          c = cross' z as block partials; the last block of each
+//                          group of chunks sums its group (fixed order)
+//   k_pcg_direction        every block sums the group sums (fixed order, so all
+//                          blocks agree bitwise), records ||r||, decides
+//                          convergence and solves mu = F^{-1} c for itself (m <=
+//                          64: a 60 x 60 factor is L2 resident), then
+//                          p_{k+1} = z + beta p_k - B mu (cg) | z - B mu (fom),
 //                          written straight into V[:, k+1]; last block advances k
+//   (wider projections and the host-stepped path combine in k_pcg_finish instead)
 //   fom: 2 x (GEMV-T over [A p_0..A p_k], divide by gamma, GEMV-N over [p_0..p_k])
 // All scalars stay on the device (rk_pcg_state); once a run converges or breaks
 // down every later kernel returns immediately, so the host can launch
@@ -39,18 +43,22 @@ int elementwise_grid(int64_t n);
 
 namespace rk {
 
-// Debug-only timeline of the fused update tail (built with -DRK_TAIL_TRACE):
-// row k % 64 holds globaltimer stamps of iteration k (see rk_debug_trace).
+// Debug-only timeline of the direction kernel's combine prologue (built with
+// -DRK_TAIL_TRACE): row k % 64 holds block 0's globaltimer stamps of
+// iteration k -- after the wait, after the group sums, after the mu solve,
+// at the end of the row loop (see rk_debug_trace).
 __device__ unsigned long long g_tail_trace[64 * 8];
 #ifdef RK_TAIL_TRACE
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#define RK_STAMP(var) const unsigned long long var = clock64()  // same block: SM cycles
+#define RK_STAMP(slot)                                                                  \
+  do {                                                                                  \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                          \
+      unsigned long long t_;                                                            \
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_));                            \
+      g_tail_trace[(st->k % 64) * 8 + (slot)] = t_;                                     \
+    }                                                                                   \
+  } while (0)
 #else
-#define RK_STAMP(var)
+#define RK_STAMP(slot)
 #endif
 
 constexpr int kUpdThreads = 256;
@@ -301,9 +309,6 @@ __global__ void __launch_bounds__(kUpdThreads, 4) k_pcg_update(const rk_pcg_plan
   __shared__ __align__(16) double zs[kProjChunk];
   __shared__ double scratch[64];
   const int64_t k = st->k;
-#ifdef RK_TAIL_TRACE
-  if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) g_tail_trace[(k % 64) * 8 + 0] = gtimer();
-#endif
   const double alpha = entry ? 0.0 : st->alpha;
   const int64_t n = P.n, m = P.m;
   const int64_t nchunks = gridDim.x;
@@ -387,38 +392,16 @@ __global__ void __launch_bounds__(kUpdThreads, 4) k_pcg_update(const rk_pcg_plan
     if (lane == 0) part[(2 + j) * nchunks + chunk] = a;
   }
   if (!fused) return;
-  RK_STAMP(t1);
-  // Fused finish (m <= kFuseMax): the last block of each group of `group`
-  // chunks (over all column groups) sums the group's partials; the last group
-  // sum to land combines the groups, then does the scalars and the mu solve.
-  // Fixed orders throughout (lanes over chunks, butterfly), so deterministic.
-  __shared__ double red[2 + kFuseMax];
-  __shared__ double ysm[kFuseMax];
+  // Deferred combine (m <= kFuseMax): the last block of each group of `group`
+  // chunks (over all column groups) sums the group's partials into
+  // gsum[v][g]; the direction kernel combines the groups. No block waits on
+  // a grid-wide chain here, so the kernel ends when its slowest group does.
   const int64_t nv = 2 + m;
   const int64_t ngroups = (nchunks + group - 1) / group;
   const int64_t g = chunk / group;
   const int64_t c0 = g * group, c1 = min(nchunks, c0 + group);
   if (!ticket_last_of(P.tickets + 8 + g, (uint32_t)((c1 - c0) * gridDim.y))) return;
-  RK_STAMP(t2);
-  double* gsum = part + nv * nchunks;  // [nv][ngroups]
-  block_row_sums(part, nchunks, nv, c0, c1, gsum + g, ngroups);
-  RK_STAMP(t3);
-  if (!ticket_last_of(P.tickets + 3, (uint32_t)ngroups)) return;
-  RK_STAMP(t4);
-  block_row_sums(gsum, ngroups, nv, 0, ngroups, red, 1);
-  __syncthreads();
-  RK_STAMP(t5);
-  const bool stop = pcg_scalars(P, entry, red);
-  RK_STAMP(t6);
-  if (!stop && m > 0) solve_factor_warps(P, red + 2, ysm, P.mu);
-#ifdef RK_TAIL_TRACE
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long* row = g_tail_trace + (k % 64) * 8;
-    const unsigned long long t7 = clock64();
-    row[1] = t1; row[2] = t2; row[3] = t3; row[4] = t4; row[5] = t5; row[6] = t6; row[7] = t7;
-  }
-#endif
+  block_row_sums(part, nchunks, nv, c0, c1, part + nv * nchunks + g, ngroups);
 }
 
 // Combine the update partials and, in the last block to finish, record ||r||,
@@ -503,25 +486,88 @@ __global__ void __launch_bounds__(256) k_pcg_musolve(const rk_pcg_plan P, int64_
 }
 
 // K5: new direction into V[:, k+1] (entry: V[:, 0]).
-__global__ void __launch_bounds__(256, kDirMinBlocks) k_pcg_direction(const rk_pcg_plan P, int entry) {
+//
+// combine = 1 (m <= kFuseMax, after a deferred update): every block first sums
+// the update's group sums, runs the scalar bookkeeping and solves mu itself.
+// The sums are in a fixed order, so every block computes bitwise the same
+// ||r||, r'z and mu; block 0 alone writes them to the state and histories.
+// beta = r'z_{k+1} / r'z_k uses rz_h[k] (written by the SpMV kernel), never
+// st->rz, which block 0 overwrites while other blocks may still start. When
+// the run has converged every block returns before the k ticket (a late block
+// that already sees st->done set by block 0 returns as well), so the ticket
+// only ever counts complete grids.
+__global__ void __launch_bounds__(256, kDirMinBlocks)
+    k_pcg_direction(const rk_pcg_plan P, int entry, int combine, int64_t nchunks, int64_t group) {
   rk_pcg_state* st = P.st;
-  pdl_wait();
-  pdl_trigger();
-  if (st->done) return;
   extern __shared__ double sm[];
-  const int64_t k = st->k;
   const int64_t m = P.m;
   double* mus = sm;              // m
   double* cps = sm + m;          // paper-beta coefficients, k+1
+  // Before the wait: warm L2 with this thread's first row of the basis (B is
+  // fixed for the run). Safe to read now: this kernel launches once every
+  // update block has passed its own pdl_wait (wait-before-trigger, common.cuh).
+  {
+    const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (combine && i0 < P.n)
+      for (int64_t j = 0; j < m; ++j) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.B + i0 + j * P.ldb));
+  }
+  pdl_wait();
+  pdl_trigger();
+  if (st->done) return;
+  RK_STAMP(0);
+  const int64_t k = st->k;
   const int paper = (P.mode == 2) && !entry;
-  for (int64_t j = threadIdx.x; j < m; j += blockDim.x) mus[j] = P.mu[j];
+  const int cg = (P.mode == 0) && !entry;
+  double beta = cg ? st->beta : 0.0, rz_next = st->rz_next;
+  if (combine) {
+    __shared__ double red[2 + kFuseMax];
+    __shared__ double ysm[kFuseMax];
+    const int64_t nv = 2 + m;
+    const int64_t ngroups = (nchunks + group - 1) / group;
+    block_row_sums(P.partials + nv * nchunks, ngroups, nv, 0, ngroups, red, 1);
+    __syncthreads();
+    RK_STAMP(1);
+    const double rr = red[0], rnorm = sqrt(rr);
+    rz_next = red[1];
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    if (entry) {
+      if (lead) {  // krylov.py:268 history[0] = ||r0|| ; :292 rz = r @ z
+        st->rr = rr;
+        P.res_h[0] = rnorm;
+        st->rz = rz_next;
+      }
+    } else {
+      const bool stop = rnorm <= st->threshold;  // krylov.py:317
+      if (lead) {
+        st->rr = rr;
+        P.res_h[k + 1] = rnorm;                  // krylov.py:314
+        if (stop) {
+          st->status = 1;
+          st->k = k + 1;
+          st->done = 1;
+        } else {
+          st->rz_next = rz_next;                 // krylov.py:321
+          st->beta = rz_next / P.rz_h[k];        // krylov.py:324 (rz_next / rz)
+          st->rz = rz_next;                      // krylov.py:340
+        }
+      }
+      if (stop) return;  // block-uniform
+      beta = cg ? rz_next / P.rz_h[k] : 0.0;
+    }
+    if (m > 0) {
+      solve_factor_warps(P, red + 2, ysm, mus);
+      __syncthreads();
+      RK_STAMP(2);
+      if (blockIdx.x == 0)
+        for (int64_t j = threadIdx.x; j < m; j += blockDim.x) P.mu[j] = mus[j];
+    }
+  } else {
+    for (int64_t j = threadIdx.x; j < m; j += blockDim.x) mus[j] = P.mu[j];
+  }
   if (paper) {
-    const double rzn = st->rz_next;
-    for (int64_t i = threadIdx.x; i <= k; i += blockDim.x) cps[i] = rzn / P.rz_h[i];
+    for (int64_t i = threadIdx.x; i <= k; i += blockDim.x) cps[i] = rz_next / P.rz_h[i];
   }
   __syncthreads();
-  const int cg = (P.mode == 0) && !entry;
-  const double beta = cg ? st->beta : 0.0;
   const double* __restrict__ pk = P.V + k * P.ldv;
   double* __restrict__ out = P.V + (entry ? k : k + 1) * P.ldv;
   const double* __restrict__ z = P.z;
@@ -550,6 +596,7 @@ __global__ void __launch_bounds__(256, kDirMinBlocks) k_pcg_direction(const rk_p
     }
     out[i] = t;
   }
+  RK_STAMP(3);
   if (!entry && ticket_last(P.tickets + 2)) {
     if (threadIdx.x == 0) st->k = k + 1;
   }
@@ -614,14 +661,19 @@ static int check_plan(const rk_pcg_plan& P, bool need_proj) {
 
 static int64_t fuse_group(int64_t nch) { return std::max<int64_t>(32, (nch + rk::kMaxGroups - 1) / rk::kMaxGroups); }
 
-static void launch_update(const rk_pcg_plan& P, int entry, cudaStream_t s, bool mark = false) {
+// deferred: the fused path of rk_pcg_entry / rk_pcg_steps (m <= kFuseMax),
+// whose direction kernel combines the update's group sums; the host-stepped
+// rk_pcg_update resolves the scalars itself (k_pcg_finish), since the host
+// reads the convergence state right after it.
+static bool deferred_combine(const rk_pcg_plan& P) { return P.m <= rk::kFuseMax; }
+
+static void launch_update(const rk_pcg_plan& P, int entry, bool defer, cudaStream_t s, bool mark = false) {
   const int64_t nch = update_chunks(P.n);
   const int64_t groups = std::max<int64_t>(1, (P.m + rk::kProjCols - 1) / rk::kProjCols);
   dim3 grid((unsigned)nch, (unsigned)groups);
-  const int fused = P.m <= rk::kFuseMax ? 1 : 0;
-  launch_pdl(rk::k_pcg_update, grid, dim3(rk::kUpdThreads), 0, s, P, entry, fused, fuse_group(nch));
+  launch_pdl(rk::k_pcg_update, grid, dim3(rk::kUpdThreads), 0, s, P, entry, defer ? 1 : 0, fuse_group(nch));
   if (mark) prof_mark(2, s);
-  if (fused) return;
+  if (defer) return;
   const unsigned fgrid = (unsigned)std::min<int64_t>(2 + P.m, 4096);
   const int wide = (P.linv_full && P.wchol > rk::kWideSolve) ? 1 : 0;
   launch_pdl(rk::k_pcg_finish, dim3(fgrid), dim3(256), finish_smem(P.m, wide ? 0 : P.wchol), s, P, entry, nch, wide);
@@ -631,9 +683,16 @@ static void launch_update(const rk_pcg_plan& P, int entry, cudaStream_t s, bool 
   }
 }
 
-static void launch_direction(const rk_pcg_plan& P, int entry, int64_t kmax, cudaStream_t s) {
+static void launch_direction(const rk_pcg_plan& P, int entry, bool combine, int64_t kmax, cudaStream_t s) {
   const size_t smem = (size_t)(P.m + (P.mode == 2 ? kmax + 1 : 0) + 1) * sizeof(double);
-  launch_pdl(rk::k_pcg_direction, dim3(elementwise_grid(P.n)), dim3(256), smem, s, P, entry);
+  const int64_t nch = update_chunks(P.n);
+  // With the combine prologue every block pays a few microseconds of
+  // dependent L2 round trips before its rows: one resident wave of blocks
+  // (kDirMinBlocks per SM) pays them once, overlapped, instead of per wave.
+  const int grid = combine ? (int)std::min<int64_t>((P.n + 255) / 256, (int64_t)sm_count() * rk::kDirMinBlocks)
+                           : elementwise_grid(P.n);
+  launch_pdl(rk::k_pcg_direction, dim3(std::max(grid, 1)), dim3(256), smem, s, P, entry, combine ? 1 : 0, nch,
+             fuse_group(nch));
   if (P.mode == 1 && !entry) {
     // two classical Gram-Schmidt sweeps against every previous direction
     // (krylov.py:333-337, block form): coef_i = (A p_i)'p / gamma_i ; p -= V coef
@@ -657,8 +716,9 @@ int debug_trace(unsigned long long* out, int64_t n) {
 int pcg_entry(const rk_pcg_plan& P, cudaStream_t s) {
   configure_once();
   if (int e = check_plan(P, true)) return e;
-  launch_update(P, 1, s);
-  launch_direction(P, 1, 0, s);
+  const bool defer = deferred_combine(P);
+  launch_update(P, 1, defer, s);
+  launch_direction(P, 1, defer, 0, s);
   return cuda_check("rk_pcg_entry");
 }
 
@@ -670,14 +730,15 @@ int pcg_steps(const rk_pcg_plan& P, int nsteps, int64_t kmax_hint, cudaStream_t 
   RK_REQUIRE(kmax_hint + 2 <= P.vcap, RK_ERR_DIMENSION, "rk_pcg_steps: kmax_hint %lld beyond capacity %lld",
              (long long)kmax_hint, (long long)P.vcap);
   if (P.mode == 1) gemv_n_smem_ok(kmax_hint + 1);
+  const bool defer = deferred_combine(P);
   for (int i = 0; i < nsteps; ++i) {
     const bool mark = prof_sample();  // 1 iteration in 8 is bracketed by events (bench only)
     if (mark) prof_mark(0, s);
     launch_spmv_pcg(P, s);
     if (mark) prof_mark(1, s);
-    launch_update(P, 0, s, mark);
+    launch_update(P, 0, defer, s, mark);
     if (mark) prof_mark(3, s);
-    launch_direction(P, 0, kmax_hint + 1, s);
+    launch_direction(P, 0, defer, kmax_hint + 1, s);
     if (mark) prof_mark(4, s);
   }
   return cuda_check("rk_pcg_steps");
@@ -693,7 +754,7 @@ int pcg_curvature(const rk_pcg_plan& P, cudaStream_t s) {
 int pcg_update(const rk_pcg_plan& P, cudaStream_t s) {
   configure_once();
   if (int e = check_plan(P, true)) return e;
-  launch_update(P, 0, s);
+  launch_update(P, 0, false, s);
   return cuda_check("rk_pcg_update");
 }
 
@@ -701,7 +762,7 @@ int pcg_direction(const rk_pcg_plan& P, int64_t kmax_hint, cudaStream_t s) {
   configure_once();
   if (int e = check_plan(P, false)) return e;
   if (P.mode == 1) gemv_n_smem_ok(kmax_hint + 1);
-  launch_direction(P, 0, kmax_hint + 1, s);
+  launch_direction(P, 0, false, kmax_hint + 1, s);
   return cuda_check("rk_pcg_direction");
 }
 
