@@ -230,3 +230,46 @@ def test_c2_sequence_matches_reference_run(pk):
         q = float(seq.C[0] @ xh)
         assert abs(q - d["q"][j]) <= 1e-10 * abs(d["q"][j])
         assert np.linalg.norm(xh[idx] - d["xs"][j]) <= 1e-8 * np.linalg.norm(d["xs"][j])
+
+
+def _reference_run(name):
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", f"{name}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"{name}.npz not generated (oracle/run_reference_seq.py)")
+    return np.load(path)
+
+
+def _run_prefix(pk, seq, cfg):
+    import warnings
+
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        return pk.run_sequence(seq, cfg, precond_factory=lambda A: pk.build_preconditioner("jacobi", A))
+
+
+def test_c3_fom_matches_reference_full_size(pk):
+    """The north-star configuration (C3: 64^3 Q1 elasticity, N = 811,200) in
+    the reference's DEFAULT mode, fom (threestage.py:68; two re-orthogonalisation
+    sweeps per iteration, krylov.py:327-337), against recykl's own run of its
+    first systems (tests/golden/c3_fom.npz, oracle/run_reference_seq.py
+    --mode fom). Full re-orthogonalisation is not rounding-chaotic, so the
+    plain north-star bar holds on every system: identical stage-3 iterations
+    and matvecs, x (at 2000 fixed indices) within 1e-8, q = c'x within 1e-10."""
+    from paper_1512_05820_b200.problems import elasticity_sequence
+
+    d = _reference_run("c3_fom")
+    p = int(d["p_done"])
+    seq = elasticity_sequence((64, 64, 64), p=p, rtol=1e-5, seed=3)
+    cfg = pk.SolverConfig(truncation=pk.TruncationConfig(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0,
+                                                         storage_cap=60, max_dim=60), mode="fom")
+    xs, reps, _ = _run_prefix(pk, seq, cfg)
+    assert [r.stage3_iters for r in reps] == d["iters"][:p].tolist()
+    assert [r.matvecs for r in reps] == d["matvecs"][:p].tolist()
+    idx = d["idx"]
+    for j, x in enumerate(xs):
+        xh = _host(x)
+        q = float(seq.C[0] @ xh)
+        assert abs(q - d["q"][j]) <= 1e-10 * abs(d["q"][j]), (j, q, d["q"][j])
+        assert np.linalg.norm(xh[idx] - d["xs"][j]) <= 1e-8 * np.linalg.norm(d["xs"][j]), j
