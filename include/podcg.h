@@ -185,6 +185,22 @@ int rk_bsr3_gather(int64_t nblk, const int32_t* perm, const double* val, double*
 /* out[s] = perm[s] >= 0 ? val[perm[s]] : 0 for s < total (the scalar SELL-32
  * values of a new matrix on a known pattern). */
 int rk_sell_gather(int64_t total, const int32_t* perm, const double* val, double* out, void* stream);
+/* Sliced-ELL view of a CSR pattern built on the device (host
+ * specification: linalg.py _bsr3_from_host / _sell1_from_host, which these
+ * replace; the reference has no such view -- its SpMV is scipy csr_matvec,
+ * recykl/linalg.py:138-148). bdim = 3: 3x3 blocks (rows 3b..3b+2 of equal
+ * length with aligned column triples), bdim = 1: scalar rows of at most
+ * max_len entries. Pass 1 (plan): len_ws[n / bdim] = (block) row lengths,
+ * sptr[nsl + 1] = slice offsets in slots (nsl = ceil(n / bdim / 32)),
+ * *nslot (device int64) = total slots, *bad (device int32) = 1 when the
+ * pattern does not qualify. Pass 2 (fill, after the caller read *nslot and
+ * allocated): scol[nslot] = (block) column per slot, perm[vals * nslot]
+ * (vals = 9 or 1) = CSR index gathered into each value slot or -1 -- the
+ * operands of rk_bsr3_gather / rk_sell_gather. */
+int rk_sell_plan(int64_t n, const int32_t* rowptr, const int32_t* col, int32_t bdim, int32_t max_len,
+                 int32_t* len_ws, int32_t* sptr, int64_t* nslot, int32_t* bad, void* stream);
+int rk_sell_fill(int64_t n, const int32_t* rowptr, const int32_t* col, int32_t bdim, const int32_t* len_ws,
+                 const int32_t* sptr, int64_t nslot, int32_t* scol, int32_t* perm, void* stream);
 /* Largest |A_ij - A_ji| over stored entries and max|A_ij| (device doubles [2]);
  * replaces the scipy transpose difference of SparseSpdMatrix._validate
  * (linalg.py:105-113). Requires sorted columns. */

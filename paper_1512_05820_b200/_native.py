@@ -119,6 +119,8 @@ _SIGNATURES = {
     "rk_csr_asymmetry": (c_i32, [ctypes.POINTER(RkCsr), c_vp, c_vp, c_i64, c_vp, c_vp]),
     "rk_sell_gather": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp]),
     "rk_bsr3_gather": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "rk_sell_plan": (c_i32, [c_i64, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "rk_sell_fill": (c_i32, [c_i64, c_vp, c_vp, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "rk_gemv_t": (c_i32, [c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "rk_gemv_n": (c_i32, [c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_i32, c_vp]),
     "rk_dot": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),

@@ -117,6 +117,10 @@ int launch_gram(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m2,
                 const double* Y2, int64_t ldy2, int64_t c1, double* G, int64_t ldg, double* ws, int64_t ws_len,
                 int64_t upper_off, cudaStream_t s);
 int64_t gram_workspace_doubles(int64_t n, int64_t m1, int64_t m2, int64_t upper_off);
+int sell_plan(int64_t n, const int32_t* rp, const int32_t* col, int32_t bdim, int32_t max_len, int32_t* len_ws,
+              int32_t* sptr, int64_t* nslot, int32_t* bad, cudaStream_t s);
+int sell_fill(int64_t n, const int32_t* rp, const int32_t* col, int32_t bdim, const int32_t* len_ws,
+              const int32_t* sptr, int64_t nslot, int32_t* scol, int32_t* perm, cudaStream_t s);
 int debug_trace(unsigned long long* out, int64_t n);
 int launch_gemm_nn(int64_t n, int64_t sdim, int64_t y, const double* S, int64_t lds, const double* C, int64_t ldc,
                    double* Out, int64_t ldo, cudaStream_t s);
@@ -235,6 +239,16 @@ int rk_sell_gather(int64_t total, const int32_t* perm, const double* val, double
   RK_REQUIRE(total >= 0, RK_ERR_DIMENSION, "rk_sell_gather: bad size");
   RK_REQUIRE(total == 0 || (perm && val && out), RK_ERR_ARG, "rk_sell_gather: null pointer");
   return rkh::launch_sell_gather(total, perm, val, out, as_stream(stream));
+}
+
+int rk_sell_plan(int64_t n, const int32_t* rowptr, const int32_t* col, int32_t bdim, int32_t max_len,
+                 int32_t* len_ws, int32_t* sptr, int64_t* nslot, int32_t* bad, void* stream) {
+  return rkh::sell_plan(n, rowptr, col, bdim, max_len, len_ws, sptr, nslot, bad, as_stream(stream));
+}
+
+int rk_sell_fill(int64_t n, const int32_t* rowptr, const int32_t* col, int32_t bdim, const int32_t* len_ws,
+                 const int32_t* sptr, int64_t nslot, int32_t* scol, int32_t* perm, void* stream) {
+  return rkh::sell_fill(n, rowptr, col, bdim, len_ws, sptr, nslot, scol, perm, as_stream(stream));
 }
 
 int rk_csr_asymmetry(const rk_csr* A, double* out2, double* ws, int64_t ws_len, uint32_t* tickets, void* stream) {

@@ -353,6 +353,49 @@ def _bsr3_from_host(rp: np.ndarray, ci: np.ndarray, n: int, device) -> _Bsr3 | N
     return _Bsr3(to(sptr), to(scol), to(perm), nslot, nblk)
 
 
+PATTERN_ON_DEVICE = os.environ.get("RK_PATTERN", "device") != "host"
+
+
+def _sell_view_on_device(dr: torch.Tensor, dc: torch.Tensor, n: int, nnz: int, bdim: int, device):
+    """rk_sell_plan + rk_sell_fill: the (3x3-block or scalar) SELL-32 arrays of
+    the uploaded pattern, bitwise those of _bsr3_from_host / _sell1_from_host;
+    None when the pattern does not qualify (two scalar reads in between)."""
+    rows = n // bdim
+    nsl = (rows + SELL_SLICE - 1) // SELL_SLICE
+    i32 = torch.int32
+    len_ws = torch.empty(max(rows, 1), dtype=i32, device=device)
+    sptr = torch.empty(nsl + 1, dtype=i32, device=device)
+    flags = torch.zeros(2, dtype=torch.int64, device=device)  # [nslot, bad]
+    bad = flags[1:].view(torch.int32)[:1]
+    s = nat.stream_ptr(device)
+    nat.check(nat.lib().rk_sell_plan(n, dr.data_ptr(), dc.data_ptr(), bdim, SELL1_MAX_ROW, len_ws.data_ptr(),
+                                     sptr.data_ptr(), flags.data_ptr(), bad.data_ptr(), s), "sell plan")
+    nslot, bad_flag = flags.tolist()
+    if bad_flag & 0xFFFFFFFF:
+        return None
+    if bdim == 1 and (nslot > SELL1_MAX_PAD * nnz or nslot >= 2**31):
+        return None
+    scol = torch.empty(max(nslot, 1), dtype=i32, device=device)
+    perm = torch.empty(max(bdim * bdim * nslot, 1), dtype=i32, device=device)
+    nat.check(nat.lib().rk_sell_fill(n, dr.data_ptr(), dc.data_ptr(), bdim, len_ws.data_ptr(), sptr.data_ptr(),
+                                     nslot, scol.data_ptr(), perm.data_ptr(), s), "sell fill")
+    return sptr, scol, perm, nslot
+
+
+def _bsr3_on_device(dr: torch.Tensor, dc: torch.Tensor, n: int, nnz: int, device) -> _Bsr3 | None:
+    if n == 0 or n % 3 or nnz == 0 or nnz % 9:
+        return None
+    v = _sell_view_on_device(dr, dc, n, nnz, 3, device)
+    return None if v is None else _Bsr3(v[0], v[1], v[2], v[3], nnz // 9)
+
+
+def _sell1_on_device(dr: torch.Tensor, dc: torch.Tensor, n: int, nnz: int, device) -> _Sell1 | None:
+    if n == 0 or nnz == 0:
+        return None
+    v = _sell_view_on_device(dr, dc, n, nnz, 1, device)
+    return None if v is None else _Sell1(v[0], v[1], v[2], v[3])
+
+
 def _pattern_known(rowptr: np.ndarray, col: np.ndarray, device) -> bool:
     """Same host pattern objects already uploaded (and checked) for this device."""
     with _pattern_cache_lock:
@@ -368,8 +411,13 @@ def _device_pattern(rowptr: np.ndarray, col: np.ndarray, device, n: int) -> _Pat
                 return p
     dr = torch.from_numpy(np.ascontiguousarray(rowptr, dtype=np.int32)).to(device)
     dc = torch.from_numpy(np.ascontiguousarray(col, dtype=np.int32)).to(device)
-    bsr = _bsr3_from_host(rowptr, col, n, device) if USE_BSR3 else None
-    sell = _sell1_from_host(rowptr, col, n, device) if (USE_SELL1 and bsr is None) else None
+    nnz = int(col.size)
+    if PATTERN_ON_DEVICE:  # ms on the device instead of seconds of numpy per pattern
+        bsr = _bsr3_on_device(dr, dc, n, nnz, device) if USE_BSR3 else None
+        sell = _sell1_on_device(dr, dc, n, nnz, device) if (USE_SELL1 and bsr is None) else None
+    else:
+        bsr = _bsr3_from_host(rowptr, col, n, device) if USE_BSR3 else None
+        sell = _sell1_from_host(rowptr, col, n, device) if (USE_SELL1 and bsr is None) else None
     p = _Pattern(dr, dc, bsr, sell)
     with _pattern_cache_lock:
         _pattern_cache.insert(0, (rowptr, col, p))

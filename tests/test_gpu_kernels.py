@@ -393,3 +393,50 @@ def test_device_spd_inverse_wide_factor(pk):
     F = L.device_spd_inverse(torch.device("cuda", 0)).cpu().numpy()
     Li = np.tril(scipy.linalg.lapack.dtrtri(L.full(), lower=1)[0])
     np.testing.assert_allclose(F, Li.T @ Li, rtol=1e-11, atol=1e-13 * np.abs(F).max())
+
+
+@pytest.mark.parametrize("case", ["elasticity", "stencil7", "poisson2d", "ragged", "long_rows"])
+def test_device_pattern_views_equal_host_builders(pk, case):
+    """the SELL-32 views built on the device (rk_sell_plan /
+    rk_sell_fill) are bitwise the host builders' arrays (slice offsets, slot
+    columns, value permutation), and both decline the same patterns."""
+    import scipy.sparse as sp
+
+    from paper_1512_05820_b200 import linalg as L
+    from paper_1512_05820_b200.problems import elasticity_sequence, laplacian3d, poisson2d_matrix
+
+    if case == "elasticity":
+        H = next(iter(elasticity_sequence((7, 5, 4), p=1))).A
+        rp, ci, n = np.asarray(H.row_offsets), np.asarray(H.col_indices), H.n
+    elif case == "stencil7":
+        H = laplacian3d(13, 9, 7)
+        rp, ci, n = np.asarray(H.row_offsets), np.asarray(H.col_indices), H.n
+    elif case == "poisson2d":
+        H = poisson2d_matrix(33)
+        rp, ci, n = np.asarray(H.row_offsets), np.asarray(H.col_indices), H.n
+    else:
+        rng = np.random.default_rng(4)
+        n = 301
+        dens = 0.01 if case == "ragged" else 0.08
+        M = sp.random(n, n, density=dens, random_state=5, format="csr") + sp.eye(n, format="csr")
+        M = (M + M.T).tocsr()
+        M.sort_indices()
+        rp, ci = M.indptr, M.indices
+    dev = torch.device("cuda", 0)
+    dr = torch.from_numpy(np.ascontiguousarray(rp, dtype=np.int32)).to(dev)
+    dc = torch.from_numpy(np.ascontiguousarray(ci, dtype=np.int32)).to(dev)
+    hb, db = L._bsr3_from_host(rp, ci, n, dev), L._bsr3_on_device(dr, dc, n, int(ci.size), dev)
+    assert (hb is None) == (db is None)
+    if hb is not None:
+        assert hb.nblk == db.nblk and hb.nreal == db.nreal
+        for a, b in ((hb.browptr, db.browptr), (hb.bcol, db.bcol), (hb.perm, db.perm)):
+            assert torch.equal(a, b)
+        return
+    hs, ds = L._sell1_from_host(rp, ci, n, dev), L._sell1_on_device(dr, dc, n, int(ci.size), dev)
+    assert (hs is None) == (ds is None), case
+    if hs is not None:
+        assert hs.nslot == ds.nslot
+        for a, b in ((hs.sptr, ds.sptr), (hs.scol, ds.scol), (hs.perm, ds.perm)):
+            assert torch.equal(a, b)
+    if case == "long_rows":
+        assert hs is None  # rows beyond SELL1_MAX_ROW keep the lanes-per-row CSR kernel
