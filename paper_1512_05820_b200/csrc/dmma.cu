@@ -500,10 +500,11 @@ static double model_cost(const GramVariant& v, int64_t m1, int64_t m2, int64_t u
 // Work plan of one Gram: variant, units (launch order) and split tiles.
 struct GramPlan {
   int which = 0;
-  int nunits = 0, nsplit = 0;
   int64_t ws_doubles = 0;
-  rk::GramUnits U;
-  rk::GramTiles T;
+  std::vector<uint64_t> code;   // units in launch order (batched kMaxUnits per launch)
+  std::vector<uint16_t> slot;
+  std::vector<uint32_t> split_ab;  // split tiles for the reduce (batched kMaxTiles per launch)
+  std::vector<uint16_t> split_first, split_count;
 };
 
 // Variant: full Grams at least 128 rows tall take 128 x 64 (fewer L2 -> SM
@@ -560,59 +561,54 @@ static int build_plan(int64_t n, int64_t m1, int64_t m2, int64_t upper_off, Gram
         total += std::max(c, floor_cost);
       }
     }
-  RK_REQUIRE((int64_t)tiles.size() <= rk::kMaxUnits, RK_ERR_DIMENSION, "rk_gram: %lld tiles exceed the unit table",
-             (long long)tiles.size());
   const int64_t slots = (int64_t)sm_count() * v.per_sm;
   const int64_t max_split = std::max<int64_t>(1, nchunk / 16);  // >= 512 rows per unit
   static const int64_t waves = [] {
     const char* e = getenv("RK_GRAM_WAVES");
     return e ? std::max(1, atoi(e)) : 4;
   }();
-  int64_t target = std::max<int64_t>((int64_t)tiles.size(), waves * slots);
+  // Wide Grams (more tiles than `waves` rounds of slots) run one unit per
+  // tile, in as many launches as the unit table needs; narrower ones split
+  // the rows (partial slots are uint16).
+  const int64_t target = std::max<int64_t>((int64_t)tiles.size(), std::min<int64_t>(waves * slots, 60000));
   static const bool uniform = [] {
     const char* e = getenv("RK_GRAM_UNIFORM");
     return e ? atoi(e) != 0 : true;
   }();
-  for (;;) {
-    int64_t units = 0;
-    const int64_t ns_u = std::min(max_split, std::max<int64_t>(1, target / (int64_t)tiles.size()));
-    for (Tile& t : tiles) {
-      t.ns = uniform ? ns_u : std::min(max_split, std::max<int64_t>(1, (target * t.cost + total / 2) / total));
-      units += t.ns;
-    }
-    if (units <= rk::kMaxUnits) break;
-    target = target * rk::kMaxUnits / units - 1;
-  }
+  const int64_t ns_u = std::min(max_split, std::max<int64_t>(1, target / (int64_t)tiles.size()));
+  for (Tile& t : tiles)
+    t.ns = uniform ? ns_u : std::min(max_split, std::max<int64_t>(1, (target * t.cost + total / 2) / total));
   // split tiles get partial slots (tile-major, so a tile's partials are contiguous)
-  int nsplit = 0, slot = 0;
-  struct U { int64_t k0; int64_t tile; uint64_t code; int slot; };
+  int64_t slot = 0;
+  struct U { int64_t k0; uint64_t code; int64_t slot; };
   static thread_local std::vector<U> units;
   units.clear();
-  for (int64_t i = 0; i < (int64_t)tiles.size(); ++i) {
-    const Tile& t = tiles[i];
+  P.split_ab.clear();
+  P.split_first.clear();
+  P.split_count.clear();
+  for (const Tile& t : tiles) {
     const bool direct = t.ns == 1;
     if (!direct) {
-      RK_REQUIRE(nsplit < rk::kMaxTiles, RK_ERR_DIMENSION, "rk_gram: too many split tiles");
-      P.T.ab[nsplit] = (uint32_t)(t.a | (t.b << 11));
-      P.T.first[nsplit] = (uint16_t)slot;
-      P.T.count[nsplit] = (uint16_t)t.ns;
-      ++nsplit;
+      RK_REQUIRE(slot + t.ns <= 65535, RK_ERR_DIMENSION, "rk_gram: too many split units");
+      P.split_ab.push_back((uint32_t)(t.a | (t.b << 11)));
+      P.split_first.push_back((uint16_t)slot);
+      P.split_count.push_back((uint16_t)t.ns);
     }
     for (int64_t q = 0; q < t.ns; ++q) {
       const int64_t k0 = nchunk * q / t.ns, k1 = nchunk * (q + 1) / t.ns;
       const uint64_t code = (uint64_t)t.a | ((uint64_t)t.b << 11) | ((uint64_t)direct << 22) | ((uint64_t)k0 << 23) |
                             ((uint64_t)k1 << 43);
-      units.push_back({k0, i, code, direct ? 0 : slot++});
+      units.push_back({k0, code, direct ? 0 : slot++});
     }
   }
   std::stable_sort(units.begin(), units.end(), [](const U& x, const U& y) { return x.k0 < y.k0; });
+  P.code.resize(units.size());
+  P.slot.resize(units.size());
   for (size_t i = 0; i < units.size(); ++i) {
-    P.U.u[i] = units[i].code;
-    P.U.slot[i] = (uint16_t)units[i].slot;
+    P.code[i] = units[i].code;
+    P.slot[i] = (uint16_t)units[i].slot;
   }
-  P.nunits = (int)units.size();
-  P.nsplit = nsplit;
-  P.ws_doubles = (int64_t)slot * v.bm * v.bn;
+  P.ws_doubles = slot * v.bm * v.bn;
   return 0;
 }
 
@@ -638,17 +634,27 @@ int launch_gram(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m2,
              RK_ERR_ARG, "rk_gram: operands need 16-byte aligned columns with even leading dimension");
   RK_REQUIRE(ldx >= n && ldy >= n && ldy2 >= n && ldg >= m1 && c1 >= 0, RK_ERR_DIMENSION,
              "rk_gram: leading dimension too small");
-  static thread_local GramPlan P;  // ~30 KB: per calling thread, never on the stack
+  static thread_local GramPlan P;  // per calling thread (re-entrant C-ABI)
+  static thread_local rk::GramUnits U;  // kernel-parameter tables, ~20 KB: never on the stack
+  static thread_local rk::GramTiles T;
   const int rc = build_plan(std::max<int64_t>(n, 1), m1, m2, upper_off, P);
   if (rc != 0) return rc;
   RK_REQUIRE(P.ws_doubles == 0 || (ws && ws_len >= P.ws_doubles), RK_ERR_ARG,
              "rk_gram: workspace too small (%lld < %lld)", (long long)ws_len, (long long)P.ws_doubles);
   const GramVariant& v = gram_variant(P.which);
-  if (P.nunits == 0) return 0;
-  v.fn<<<P.nunits, v.threads, v.smem, s>>>(n, m1, X, ldx, m2, Y, ldy, Y2, ldy2, c1, G, ldg, ws, upper_off, P.U);
-  rkh::note_launch();
-  if (P.nsplit) {
-    v.reduce<<<P.nsplit, 256, 0, s>>>(m1, m2, ws, G, ldg, P.T);
+  for (size_t u0 = 0; u0 < P.code.size(); u0 += rk::kMaxUnits) {
+    const size_t cnt = std::min<size_t>(rk::kMaxUnits, P.code.size() - u0);
+    std::copy_n(P.code.begin() + u0, cnt, U.u);
+    std::copy_n(P.slot.begin() + u0, cnt, U.slot);
+    v.fn<<<(unsigned)cnt, v.threads, v.smem, s>>>(n, m1, X, ldx, m2, Y, ldy, Y2, ldy2, c1, G, ldg, ws, upper_off, U);
+    rkh::note_launch();
+  }
+  for (size_t t0 = 0; t0 < P.split_ab.size(); t0 += rk::kMaxTiles) {
+    const size_t cnt = std::min<size_t>(rk::kMaxTiles, P.split_ab.size() - t0);
+    std::copy_n(P.split_ab.begin() + t0, cnt, T.ab);
+    std::copy_n(P.split_first.begin() + t0, cnt, T.first);
+    std::copy_n(P.split_count.begin() + t0, cnt, T.count);
+    v.reduce<<<(unsigned)cnt, 256, 0, s>>>(m1, m2, ws, G, ldg, T);
     rkh::note_launch();
   }
   return cuda_check("rk_gram");

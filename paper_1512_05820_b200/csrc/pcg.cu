@@ -64,7 +64,8 @@ __device__ unsigned long long g_tail_trace[64 * 8];
 constexpr int kUpdThreads = 256;
 constexpr int kProjChunk = 1024;                 // rows per update block
 constexpr int kProjCols = 32;                    // cross columns per update block (4 per warp)
-constexpr int kMaxProj = 4096;                   // projection width of the fused path (C4: ~3000)
+constexpr int64_t kMaxProj = 65535 * 32;          // projection width: the update grid's y extent (C4: ~3000)
+constexpr int64_t kStageMu = 16384;              // mu / reduced sums staged in shared memory up to this width
 constexpr int kStageFactor = 96;                 // Linv staged in shared memory up to this width
 #ifndef RK_DIR_UNROLL
 #define RK_DIR_UNROLL 12
@@ -412,11 +413,15 @@ __global__ void __launch_bounds__(kUpdThreads, 4) k_pcg_update(const rk_pcg_plan
 // memory before waiting on the update kernel (overlapping its tail).
 __global__ void __launch_bounds__(256) k_pcg_finish(const rk_pcg_plan P, int entry, int64_t nchunks, int wide) {
   rk_pcg_state* st = P.st;
-  extern __shared__ double dyn[];      // Ls[w*w] (staged) | red[2 + m] | ysm[2 w]
+  extern __shared__ double dyn[];      // Ls[w*w] (staged) | red[2 + m] (or [2]) | ysm[2 w]
   __shared__ double scratch[32];
   const int64_t m = P.m, w = P.wchol;
   const int64_t nv = 2 + m;
   const bool staged = w > 0 && w <= kStageFactor;
+  // the reduced sums the last block needs in shared memory: all of them for
+  // its own mu solve, only ||r||^2 and r'z when k_pcg_musolve solves (wide)
+  // or when they would not fit (the solve then reads c from the global sums)
+  const bool stage_red = !wide && nv <= kStageMu;
   double* Ls = dyn;
   double* red = dyn + (staged ? w * w : 0);
   if (staged) {
@@ -440,10 +445,11 @@ __global__ void __launch_bounds__(256) k_pcg_finish(const rk_pcg_plan P, int ent
   }
   if (!ticket_last(P.tickets + 1)) return;  // fences thread 0's sums before the ticket
   __threadfence();
-  for (int64_t j = threadIdx.x; j < nv; j += blockDim.x) red[j] = __ldcg(sums + j);
+  const int64_t nred = stage_red ? nv : 2;
+  for (int64_t j = threadIdx.x; j < nred; j += blockDim.x) red[j] = __ldcg(sums + j);
   __syncthreads();
   if (pcg_scalars(P, entry, red) || m == 0 || wide) return;  // wide: k_pcg_musolve follows
-  solve_factor(P, red + 2, red + nv, staged ? Ls : nullptr, P.mu);
+  solve_factor(P, stage_red ? red + 2 : sums + 2, red + nred, staged ? Ls : nullptr, P.mu);
 }
 
 // mu = F^{-1} c for wide dense factors (w > kWideSolve, F^{-1} held full and
@@ -501,8 +507,9 @@ __global__ void __launch_bounds__(256, kDirMinBlocks)
   rk_pcg_state* st = P.st;
   extern __shared__ double sm[];
   const int64_t m = P.m;
-  double* mus = sm;              // m
-  double* cps = sm + m;          // paper-beta coefficients, k+1
+  const int64_t mstage = m <= kStageMu ? m : 0;
+  double* mus = sm;              // m (staged widths)
+  double* cps = sm + mstage;     // paper-beta coefficients, k+1
   // Before the wait: warm L2 with this thread's first row of the basis (B is
   // fixed for the run). Safe to read now: this kernel launches once every
   // update block has passed its own pdl_wait (wait-before-trigger, common.cuh).
@@ -561,9 +568,10 @@ __global__ void __launch_bounds__(256, kDirMinBlocks)
       if (blockIdx.x == 0)
         for (int64_t j = threadIdx.x; j < m; j += blockDim.x) P.mu[j] = mus[j];
     }
-  } else {
+  } else if (m <= kStageMu) {
     for (int64_t j = threadIdx.x; j < m; j += blockDim.x) mus[j] = P.mu[j];
   }
+  const double* __restrict__ muv = (combine || m <= kStageMu) ? mus : P.mu;  // wider: read in place (L2)
   if (paper) {
     for (int64_t i = threadIdx.x; i <= k; i += blockDim.x) cps[i] = rz_next / P.rz_h[i];
   }
@@ -586,9 +594,9 @@ __global__ void __launch_bounds__(256, kDirMinBlocks)
 #pragma unroll
         for (int u = 0; u < kDirUnroll; ++u) b[u] = __ldcs(row + (j + u) * P.ldb);
 #pragma unroll
-        for (int u = 0; u < kDirUnroll; ++u) s = fma(b[u], mus[j + u], s);
+        for (int u = 0; u < kDirUnroll; ++u) s = fma(b[u], muv[j + u], s);
       }
-      for (; j < m; ++j) s = fma(__ldcs(row + j * P.ldb), mus[j], s);
+      for (; j < m; ++j) s = fma(__ldcs(row + j * P.ldb), muv[j], s);
       t = __dsub_rn(t, s);
     }
     if (paper) {                                          // krylov.py:329-331, same order
@@ -611,9 +619,10 @@ bool prof_sample();
 
 static int64_t update_chunks(int64_t n) { return std::max<int64_t>(1, (n + rk::kProjChunk - 1) / rk::kProjChunk); }
 
-static size_t finish_smem(int64_t m, int64_t wchol) {
+static size_t finish_smem(int64_t m, int64_t wchol, bool wide) {
   const int64_t staged = (wchol > 0 && wchol <= rk::kStageFactor) ? wchol * wchol : 0;
-  return (size_t)(staged + 2 + m + 2 * wchol) * sizeof(double);
+  const int64_t red = (!wide && 2 + m <= rk::kStageMu) ? 2 + m : 2;
+  return (size_t)(staged + red + (wide ? 0 : 2 * wchol)) * sizeof(double);
 }
 
 int64_t pcg_workspace_doubles(int64_t n, int64_t m, int64_t vcap) {
@@ -676,7 +685,8 @@ static void launch_update(const rk_pcg_plan& P, int entry, bool defer, cudaStrea
   if (defer) return;
   const unsigned fgrid = (unsigned)std::min<int64_t>(2 + P.m, 4096);
   const int wide = (P.linv_full && P.wchol > rk::kWideSolve) ? 1 : 0;
-  launch_pdl(rk::k_pcg_finish, dim3(fgrid), dim3(256), finish_smem(P.m, wide ? 0 : P.wchol), s, P, entry, nch, wide);
+  launch_pdl(rk::k_pcg_finish, dim3(fgrid), dim3(256), finish_smem(P.m, wide ? 0 : P.wchol, wide), s, P, entry, nch,
+             wide);
   if (wide) {
     const unsigned mgrid = (unsigned)std::min<int64_t>((P.m + 7) / 8, (int64_t)sm_count() * 8);
     launch_pdl(rk::k_pcg_musolve, dim3(mgrid), dim3(256), 0, s, P, nch);
@@ -684,7 +694,8 @@ static void launch_update(const rk_pcg_plan& P, int entry, bool defer, cudaStrea
 }
 
 static void launch_direction(const rk_pcg_plan& P, int entry, bool combine, int64_t kmax, cudaStream_t s) {
-  const size_t smem = (size_t)(P.m + (P.mode == 2 ? kmax + 1 : 0) + 1) * sizeof(double);
+  const size_t smem =
+      (size_t)((P.m <= rk::kStageMu ? P.m : 0) + (P.mode == 2 ? kmax + 1 : 0) + 1) * sizeof(double);
   const int64_t nch = update_chunks(P.n);
   // With the combine prologue every block pays a few microseconds of
   // dependent L2 round trips before its rows: one resident wave of blocks

@@ -156,18 +156,21 @@ def test_batching_does_not_change_results(pk):
     assert np.array_equal(_np(a.x), _np(b.x))  # deterministic reductions: bitwise
 
 
-def test_wide_projection_matches_oracle(pk):
+@pytest.mark.parametrize("nx,width", [(64, 300), (96, 4500)])
+def test_wide_projection_matches_oracle(pk, nx, width):
     """Projection width 300 (> the 256 above which mu = F^{-1} c is spread over
-    the whole GPU by k_pcg_musolve instead of the finish kernel's last block):
-    same iteration count and solution as the oracle on C1's Poisson matrix."""
+    the whole GPU by k_pcg_musolve instead of the finish kernel's last block)
+    and 4500 (beyond the former 4096-column limit of the fused path; the
+    reference has none): same iteration count and solution as the oracle on
+    a 2-D Poisson matrix."""
     from oracle import recycle_oracle as O
     from paper_1512_05820_b200.problems import poisson2d_matrix
 
-    L = poisson2d_matrix(64)
+    L = poisson2d_matrix(nx)
     A = pk.SparseSpdMatrix(L.n, L.row_offsets, L.col_indices, L.values)
     As = O.as_csr(L)
     rng = np.random.default_rng(11)
-    Y = np.linalg.qr(rng.standard_normal((L.n, 300)))[0]
+    Y = np.linalg.qr(rng.standard_normal((L.n, width)))[0]
     b = rng.standard_normal(L.n)
     yhat0 = np.linalg.solve(Y.T @ (As @ Y), Y.T @ b)
     M = pk.build_preconditioner("jacobi", A)
