@@ -273,3 +273,74 @@ def test_c3_fom_matches_reference_full_size(pk):
         q = float(seq.C[0] @ xh)
         assert abs(q - d["q"][j]) <= 1e-10 * abs(d["q"][j]), (j, q, d["q"][j])
         assert np.linalg.norm(xh[idx] - d["xs"][j]) <= 1e-8 * np.linalg.norm(d["xs"][j]), j
+
+
+def test_c4_prefix_matches_reference(pk):
+    """C4 (BASELINE configs[3]: 128x128x64 Q1 elasticity, K + M/dt^2, N =
+    3,219,840, one invariant matrix, rtol 1e-6, pod-a-rbf cap 3000) against
+    recykl's own run of its first systems (tests/golden/c4_prefix.npz,
+    oracle/run_reference_seq.py --workload c4). System 1 is plain Jacobi PCG,
+    system 2 the stage-1 direct projection onto the 125 stored directions
+    followed by augmented CG. The north-star bar on every system: identical
+    stage-3 iterations and matvecs, x (at 2000 fixed indices) within 1e-8,
+    q = c'x within 1e-10."""
+    from paper_1512_05820_b200.problems import elasticity_sequence
+
+    d = _reference_run("c4_prefix")
+    p = int(d["p_done"])
+    seq = elasticity_sequence((128, 128, 64), p=p, rtol=1e-6, seed=4, dynamic=True)
+    cfg = pk.SolverConfig(truncation=pk.TruncationConfig(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0,
+                                                         storage_cap=3000, max_dim=60), mode="cg")
+    xs, reps, _ = _run_prefix(pk, seq, cfg)
+    assert [r.stage3_iters for r in reps] == d["iters"][:p].tolist()
+    assert [r.matvecs for r in reps] == d["matvecs"][:p].tolist()
+    assert [r.precond_applies for r in reps] == d["precond"][:p].tolist()
+    assert [r.basis_dim for r in reps] == d["basis_dim"][:p].tolist()
+    idx = d["idx"]
+    for j, x in enumerate(xs):
+        xh = _host(x)
+        q = float(seq.C[0] @ xh)
+        assert abs(q - d["q"][j]) <= 1e-10 * abs(d["q"][j]), (j, q, d["q"][j])
+        assert np.linalg.norm(xh[idx] - d["xs"][j]) <= 1e-8 * np.linalg.norm(d["xs"][j]), j
+
+
+def test_c5_full_size_matches_reference(pk):
+    """C5 (BASELINE configs[4]) at full size: A = 7-point Laplacian on
+    128 x 128 x 256 (N = 4,194,304), S = 256 N(0,1) snapshots from the same
+    seeded host generator, G = assemble_gram(A, S) and pod_evd_from_gram(G, S,
+    1, 1.0) on the device against recykl's own run (tests/golden/
+    c5_full_m256.npz, oracle/run_reference_c5.py; linalg.py:160-174,
+    pod.py:123-131). Bar: G's diagonal and sampled entries within 1e-12
+    relative, sigma within 1e-10, the same retained dimension y, Phi at 2000
+    rows within 1e-8 (column signs are LAPACK's choice: aligned first)."""
+    from paper_1512_05820_b200.linalg import as_block, assemble_gram
+    from paper_1512_05820_b200.problems import laplacian3d, snapshot_matrix
+
+    d = _reference_run("c5_full_m256")
+    m = int(d["m"])
+    L = laplacian3d(128, 128, 256)
+    A = pk.SparseSpdMatrix(L.n, L.row_offsets, L.col_indices, L.values)
+    S = as_block(snapshot_matrix(L.n, m, seed=int(d["seed"])))
+    G, AS = assemble_gram(A, S)
+    del AS
+    Gh = _host(G)
+    np.testing.assert_allclose(np.diag(Gh), d["G_diag"], rtol=1e-12)
+    ij = d["G_ij"]
+    np.testing.assert_allclose(Gh[ij[:, 0], ij[:, 1]], d["G_ij_val"], rtol=1e-12,
+                               atol=1e-12 * np.abs(d["G_diag"]).max())
+    import warnings
+
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        res = pk.pod_evd_from_gram(G, S, np.ones(m), 1.0)
+    assert res.y == int(d["y"])
+    np.testing.assert_allclose(res.singular_values, d["sigma"], rtol=1e-10)
+    rows = torch.from_numpy(d["rows"]).to("cuda")
+    phi = res.columns[rows].cpu().numpy()
+    ref = d["phi_rows"][:, :phi.shape[1]]
+    sign = np.sign(np.sum(phi * ref, axis=0))
+    assert np.all(sign != 0)
+    phi = phi * sign
+    assert np.linalg.norm(phi - ref) <= 1e-8 * np.linalg.norm(ref)
+    colerr = np.linalg.norm(phi - ref, axis=0) / np.linalg.norm(ref, axis=0)
+    assert colerr.max() <= 1e-8, colerr.max()
