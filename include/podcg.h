@@ -154,6 +154,18 @@ int rk_pcg_entry(const rk_pcg_plan* plan, void* stream);
 /* nsteps full iterations for a CSR operator (K1,K3,K4,K5 per step); steps after
  * convergence/breakdown are no-ops, so the host may overshoot. */
 int rk_pcg_steps(const rk_pcg_plan* plan, int32_t nsteps, int64_t kmax_hint, void* stream);
+/* Persistent single-cluster solver for small systems (pcg_cluster.cu): ONE
+ * thread-block cluster of <= 16 CTAs runs the iterations of rk_pcg_steps
+ * (same statements, cg / fom / paper beta) from st->k until convergence,
+ * breakdown or k == kend, with the scalars exchanged through distributed
+ * shared memory and no further launches (krylov.py:300-340 for latency-bound
+ * sizes such as BASELINE configs[0]). Eligible: a CSR operator, n <=
+ * rk_pcg_cluster_max_rows(), m <= 64, fom keeps A p_k (ldav > 0); needs
+ * kend + 1 <= vcap. Like rk_pcg_steps it follows rk_pcg_entry and may be
+ * called again to continue (e.g. after the caller grew V). */
+int rk_pcg_cluster_eligible(const rk_pcg_plan* plan);
+int64_t rk_pcg_cluster_max_rows(void);
+int rk_pcg_run_cluster(const rk_pcg_plan* plan, int64_t kend, void* stream);
 /* Generic-operator pieces (ReducedSpdOperator, krylov.py:60-83): the caller writes
  * A p_k into AV column k (or the AV vector), then calls these three in order. */
 int rk_pcg_curvature(const rk_pcg_plan* plan, void* stream);
@@ -276,6 +288,9 @@ int64_t rk_launch_count(void);
  * tail (iteration k in row k % 64); zeros unless built with -DRK_TAIL_TRACE. */
 int rk_debug_trace(uint64_t* out, int64_t n);
 int rk_profile_end(double* ms4, int64_t* count4);  /* slots: spmv, update, finish, direction */
+/* After rk_profile_end: total milliseconds and launches of the persistent
+ * cluster solver (rk_pcg_run_cluster) between begin and end. */
+int rk_profile_cluster(double* ms, int64_t* launches);
 
 #ifdef __cplusplus
 }

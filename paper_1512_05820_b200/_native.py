@@ -110,6 +110,9 @@ _SIGNATURES = {
     "rk_gram_upper_workspace_doubles": (c_i64, [c_i64, c_i64, c_i64, c_i64]),
     "rk_pcg_entry": (c_i32, [ctypes.POINTER(RkPcgPlan), c_vp]),
     "rk_pcg_steps": (c_i32, [ctypes.POINTER(RkPcgPlan), c_i32, c_i64, c_vp]),
+    "rk_pcg_cluster_eligible": (c_i32, [ctypes.POINTER(RkPcgPlan)]),
+    "rk_pcg_cluster_max_rows": (c_i64, []),
+    "rk_pcg_run_cluster": (c_i32, [ctypes.POINTER(RkPcgPlan), c_i64, c_vp]),
     "rk_pcg_curvature": (c_i32, [ctypes.POINTER(RkPcgPlan), c_vp]),
     "rk_pcg_update": (c_i32, [ctypes.POINTER(RkPcgPlan), c_vp]),
     "rk_pcg_direction": (c_i32, [ctypes.POINTER(RkPcgPlan), c_i64, c_vp]),
@@ -140,6 +143,7 @@ _SIGNATURES = {
     "rk_debug_trace": (c_i32, [ctypes.POINTER(ctypes.c_uint64), c_i64]),
     "rk_ssor_apply": (c_i32, [ctypes.POINTER(RkCsr), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp]),
     "rk_profile_end": (c_i32, [ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64)]),
+    "rk_profile_cluster": (c_i32, [ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64)]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)

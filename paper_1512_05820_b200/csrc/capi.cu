@@ -56,6 +56,8 @@ struct ProfState {
   size_t used = 0;
 };
 static ProfState g_prof;
+double g_cluster_ms = 0.0;  // rk_profile_end: total ms / launches of the cluster solver (slots 8 -> 9)
+int64_t g_cluster_n = 0;
 
 static std::atomic<int64_t> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -94,6 +96,9 @@ int launch_ssor_apply(const rk_csr& A, const double* dw, const double* d, const 
                       int* flags, unsigned int* counters, int epoch, cudaStream_t s);
 int pcg_entry(const rk_pcg_plan& P, cudaStream_t s);
 int pcg_steps(const rk_pcg_plan& P, int nsteps, int64_t kmax_hint, cudaStream_t s);
+int pcg_cluster_eligible(const rk_pcg_plan& P);
+int pcg_cluster_run(const rk_pcg_plan& P, int64_t kend, cudaStream_t s);
+int64_t pcg_cluster_max_rows();
 int pcg_curvature(const rk_pcg_plan& P, cudaStream_t s);
 int pcg_update(const rk_pcg_plan& P, cudaStream_t s);
 int pcg_direction(const rk_pcg_plan& P, int64_t kmax_hint, cudaStream_t s);
@@ -181,6 +186,17 @@ int rk_pcg_steps(const rk_pcg_plan* plan, int32_t nsteps, int64_t kmax_hint, voi
   RK_REQUIRE(plan, RK_ERR_ARG, "rk_pcg_steps: null plan");
   if (int e = rkh::check_csr(&plan->A)) return e;
   return rkh::pcg_steps(*plan, nsteps, kmax_hint, as_stream(stream));
+}
+
+int rk_pcg_cluster_eligible(const rk_pcg_plan* plan) { return plan ? rkh::pcg_cluster_eligible(*plan) : 0; }
+
+int64_t rk_pcg_cluster_max_rows(void) { return rkh::pcg_cluster_max_rows(); }
+
+int rk_pcg_run_cluster(const rk_pcg_plan* plan, int64_t kend, void* stream) {
+  RK_REQUIRE(plan, RK_ERR_ARG, "rk_pcg_run_cluster: null plan");
+  if (int e = rkh::check_csr(&plan->A)) return e;
+  if (int e = rkh::pcg_cluster_run(*plan, kend, as_stream(stream))) return e;
+  return rkh::cuda_check("rk_pcg_run_cluster");
 }
 
 int rk_pcg_curvature(const rk_pcg_plan* plan, void* stream) {
@@ -362,6 +378,12 @@ int rk_debug_trace(uint64_t* out, int64_t n) {
 int64_t rk_launch_count(void) { return rkh::g_launches.load(std::memory_order_relaxed); }
 
 // Start collecting per-kernel event timings of rk_pcg_steps.
+int rk_profile_cluster(double* ms, int64_t* launches) {
+  *ms = rkh::g_cluster_ms;
+  *launches = rkh::g_cluster_n;
+  return RK_OK;
+}
+
 int rk_profile_begin(void) {
   rkh::g_prof.on = true;
   rkh::g_prof.used = 0;
@@ -380,8 +402,18 @@ int rk_profile_end(double* ms4, int64_t* count4) {
   auto& mk = rkh::g_prof.marks;
   if (!mk.empty() && cudaEventSynchronize(mk.back().second) != cudaSuccess) return rkh::cuda_check("rk_profile_end");
   std::vector<float> dur(mk.size(), -1.f), spmv;
+  rkh::g_cluster_ms = 0.0;
+  rkh::g_cluster_n = 0;
   for (size_t i = 0; i + 1 < mk.size(); ++i) {
     const int a = mk[i].first, b = mk[i + 1].first;
+    if (a == 8 && b == 9) {  // one persistent cluster solve (pcg_cluster.cu)
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, mk[i].second, mk[i + 1].second) == cudaSuccess) {
+        rkh::g_cluster_ms += ms;
+        rkh::g_cluster_n += 1;
+      }
+      continue;
+    }
     if (b == a + 1 && a < 4) {
       float ms = 0.f;
       if (cudaEventElapsedTime(&ms, mk[i].second, mk[i + 1].second) == cudaSuccess) {

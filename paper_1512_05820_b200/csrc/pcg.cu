@@ -23,6 +23,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "pcg_device.cuh"
 
 namespace rkh {
 void launch_spmv_pcg(const rk_pcg_plan& P, cudaStream_t s);
@@ -76,7 +77,6 @@ constexpr int kStageFactor = 96;                 // Linv staged in shared memory
 constexpr int kDirUnroll = RK_DIR_UNROLL;          // B loads in flight per row in the direction kernel
 constexpr int kDirMinBlocks = RK_DIR_MINB;
 constexpr int kWideSolve = 256;                  // dense factors wider than this: mu on the whole GPU
-constexpr int kFuseMax = 64;                     // widths whose finish runs in the update kernel's tail
 constexpr int kMaxGroups = 256;                  // chunk groups of the fused two-level combine
 
 // mu = F^{-1} c with F = blockdiag(L L', diag(sqd)^2) (krylov.py:119-132
@@ -123,90 +123,6 @@ __device__ void solve_factor(const rk_pcg_plan& P, const double* c, double* ysm,
   for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
     if (i < w) mu[i] = ysm[i + w];
     else {
-      const double d = P.sqd[i - w];
-      mu[i] = c[i] / (d * d);
-    }
-  }
-}
-
-// mu = F^{-1} c for w <= kFuseMax with one 256-thread block: warp q-rows
-// (rows warp + 8q), lanes over the row's entries, butterfly sums. Each batch of
-// 32 entries issues all its rows' loads before any fma, so a triangular
-// mat-vec costs ceil(w / 32) L2 round trips rather than one per row.
-__device__ void solve_factor_warps(const rk_pcg_plan& P, const double* c, double* y, double* mu) {
-  constexpr int R = kFuseMax / 8;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int w = (int)P.wchol, m = (int)P.m;
-  const int64_t ldl = P.ldl;
-  const double* __restrict__ L = P.L;
-  double a[R], lv[R];
-#pragma unroll
-  for (int q = 0; q < R; ++q) a[q] = 0.0;
-  if (P.linv_full) {  // mu_i = sum_j Finv[j, i] c_j (column i: coalesced), one pass
-    for (int t = 0; 32 * t < w; ++t) {
-      const int j = lane + 32 * t;
-#pragma unroll
-      for (int q = 0; q < R; ++q) {
-        const int i = warp + 8 * q;
-        lv[q] = (i < w && j < w) ? __ldg(L + j + (int64_t)i * ldl) : 0.0;
-      }
-      const double cj = j < w ? c[j] : 0.0;
-#pragma unroll
-      for (int q = 0; q < R; ++q) a[q] = fma(lv[q], cj, a[q]);
-    }
-    warp_sum_n(a);
-#pragma unroll
-    for (int q = 0; q < R; ++q) {
-      const int i = warp + 8 * q;
-      if (lane == 0 && i < w) mu[i] = a[q];
-    }
-    for (int i = threadIdx.x; i < m; i += blockDim.x) {
-      if (i >= w) {
-        const double d = P.sqd[i - w];
-        mu[i] = c[i] / (d * d);
-      }
-    }
-    return;
-  }
-  for (int t = 0; 32 * t < w; ++t) {  // y_i = sum_{j <= i} Linv[i, j] c_j
-    const int j = lane + 32 * t;
-#pragma unroll
-    for (int q = 0; q < R; ++q) {
-      const int i = warp + 8 * q;
-      lv[q] = (i < w && j <= i) ? __ldg(L + i + (int64_t)j * ldl) : 0.0;
-    }
-    const double cj = j < w ? c[j] : 0.0;
-#pragma unroll
-    for (int q = 0; q < R; ++q) a[q] = fma(lv[q], cj, a[q]);
-  }
-  warp_sum_n(a);
-#pragma unroll
-  for (int q = 0; q < R; ++q) {
-    const int i = warp + 8 * q;
-    if (lane == 0 && i < w) y[i] = a[q];
-    a[q] = 0.0;
-  }
-  __syncthreads();
-  for (int t = 0; 32 * t < w; ++t) {  // mu_i = sum_{j >= i} Linv[j, i] y_j (column i: coalesced)
-#pragma unroll
-    for (int q = 0; q < R; ++q) {
-      const int i = warp + 8 * q;
-      const int j = lane + 32 * t;
-      lv[q] = (i < w && j >= i && j < w) ? __ldg(L + j + (int64_t)i * ldl) : 0.0;
-    }
-    const int j = lane + 32 * t;
-    const double yj = j < w ? y[j] : 0.0;
-#pragma unroll
-    for (int q = 0; q < R; ++q) a[q] = fma(lv[q], yj, a[q]);
-  }
-  warp_sum_n(a);
-#pragma unroll
-  for (int q = 0; q < R; ++q) {
-    const int i = warp + 8 * q;
-    if (lane == 0 && i < w) mu[i] = a[q];
-  }
-  for (int i = threadIdx.x; i < m; i += blockDim.x) {
-    if (i >= w) {
       const double d = P.sqd[i - w];
       mu[i] = c[i] / (d * d);
     }
@@ -635,6 +551,8 @@ int64_t pcg_workspace_doubles(int64_t n, int64_t m, int64_t vcap) {
   need = std::max<int64_t>(need, (2 + m) * (nch + std::max<int64_t>(1, (nch + 31) / 32)));
   // fom gemv-t partials: chunks x vcap
   need = std::max<int64_t>(need, gemv_nchunks(n) * std::max<int64_t>(vcap, 1));
+  // cluster solver (pcg_cluster.cu), fom: two sweeps x 16 CTAs x (vcap + 1) partials
+  need = std::max<int64_t>(need, 2 * 16 * (vcap + 1));
   return need;
 }
 

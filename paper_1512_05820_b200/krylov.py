@@ -804,8 +804,27 @@ def _result(run: _Run, k: int, converged: bool) -> AugmentedPcgResult:
     return res
 
 
+def _drive_cluster(run: _Run, max_iter: int):
+    """Small systems: the persistent single-cluster solver (rk_pcg_run_cluster)
+    runs to convergence in one launch; it is relaunched from the device state
+    only when the direction block must grow first."""
+    lib = nat.lib()
+    k = 0
+    while True:
+        if run.vcap - 2 <= k:
+            run.ensure(k + 66)  # doubles the block
+        kend = min(max_iter, run.vcap - 2)
+        nat.check(lib.rk_pcg_run_cluster(run.plan, kend, nat.stream_ptr(run.device)), "augmented_pcg cluster")
+        st = run.read_state()
+        if st.done or int(st.k) >= max_iter:
+            return int(st.k), int(st.status)
+        k = int(st.k)
+
+
 def _drive_fused(run: _Run, max_iter: int, batch: int | None):
     """Batched device iterations; one 96-byte state read per batch."""
+    if nat.lib().rk_pcg_cluster_eligible(run.plan):
+        return _drive_cluster(run, max_iter)
     launched = 0
     step = 4
     cap = int(batch) if batch else 64

@@ -207,3 +207,43 @@ def test_wide_stage1_cholesky_on_device(pk):
     with pytest.raises(pk.NotPositiveDefinite) as e_host:
         pk.dense_cholesky(Gbad)
     assert e_dev.value.pivot == e_host.value.pivot == 300
+
+
+def test_reduced_spd_operator_matches_reference_statements(pk):
+    """ReducedSpdOperator (krylov.py:60-83) on the device: p -> Y'(A(Yp)) by
+    GEMV-N, SpMV, GEMV-T equals the reference's statements, charges one matvec
+    per application and records the full products; augmented_pcg over it (the
+    reference's stage-2 / phi=1 inner solve, threestage.py:143-220) takes the
+    oracle's iterations and reaches its solution."""
+    import torch
+
+    from oracle import recycle_oracle as O
+    from paper_1512_05820_b200.problems import poisson2d_matrix
+
+    L = poisson2d_matrix(32)
+    As = O.as_csr(L)
+    A = pk.SparseSpdMatrix(L.n, L.row_offsets, L.col_indices, L.values)
+    rng = np.random.default_rng(5)
+    Y = np.linalg.qr(rng.standard_normal((L.n, 30)))[0]
+    sink = pk.InstrumentationSink()
+    op = pk.ReducedSpdOperator(A, Y, sink, record_products=True)
+    p = rng.standard_normal(30)
+    got = _np(op.apply(p))
+    want = Y.T @ (As @ (Y @ p))
+    assert np.linalg.norm(got - want) <= 1e-13 * np.linalg.norm(want)
+    assert sink.matvecs == 1
+    full = _np(op.full_products_block())
+    assert full.shape == (L.n, 1)
+    assert np.linalg.norm(full[:, 0] - As @ (Y @ p)) <= 1e-13 * np.linalg.norm(full[:, 0])
+    assert isinstance(op.reduced_products[0], torch.Tensor)
+
+    bhat = Y.T @ rng.standard_normal(L.n)
+    sink2 = pk.InstrumentationSink()
+    op2 = pk.ReducedSpdOperator(A, Y, sink2)
+    res = pk.augmented_pcg(op2, bhat, tol=1e-10 * np.linalg.norm(bhat), mode="cg", max_iter=200)
+    t = O.Tally()
+    ref = O.aug_pcg(O.ReducedOp(As, Y, t), bhat, tol=1e-10 * np.linalg.norm(bhat), mode="cg", max_iter=200,
+                    tally=t)
+    assert res.k == ref.k
+    assert sink2.matvecs == t.matvecs
+    assert np.linalg.norm(_np(res.x) - ref.x) <= 1e-10 * np.linalg.norm(ref.x)
