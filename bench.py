@@ -245,6 +245,11 @@ def _shared_host_specs(args, seq, rank, world, dist):
         return list(seq)
     from paper_1512_05820_b200.problems import HostCsr, LinearSystemSpec
 
+    specs = list(seq)
+    if getattr(specs[0].A, "affine", None) is not None:
+        return specs  # C3: two value arrays per rank (1 GB), every system's values formed on the device
+    del specs
+
     base = os.path.join(os.environ.get("RK_BENCH_SHM", "/tmp"), f"rk_bench_{args.workload}_{args.grid}_{args.systems}")
     if rank == 0:
         specs = list(seq)
@@ -361,8 +366,19 @@ def run_b200(args, rank, world, dist):
         torch.cuda.empty_cache()
     if not args.no_e2e:
         hseq = pk.SystemSequence(n, host_specs, C=seq.C)
-        h2d = sum(s.b.nbytes for s in host_specs) + sum({id(s.A): s.A.values.nbytes for s in host_specs}.values())
+        # matrix bytes that cross PCIe: an affine sequence (C3) uploads its two
+        # value arrays once, any other one every distinct matrix's values
+        parts = {}
+        for s in host_specs:
+            aff = getattr(s.A, "affine", None)
+            for arr in (aff[:2] if aff is not None else (s.A.values,)):
+                parts[id(arr)] = arr.nbytes
+        h2d = sum(s.b.nbytes for s in host_specs) + sum(parts.values())
         d2h = n * 8 * len(host_specs)
+        from paper_1512_05820_b200 import linalg as _L
+
+        with _L._affine_cache_lock:
+            _L._affine_cache.clear()  # the `value` leg's setup uploaded them: the e2e run pays its own H2D
         barrier(dist)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -374,10 +390,7 @@ def run_b200(args, rank, world, dist):
         # cold: the same call once more with the pattern cache emptied, so the
         # int32 pattern upload and the SELL view build (on the device) are paid
         # inside the timed region, as by a first drop-in call in a fresh process
-        from paper_1512_05820_b200 import linalg as _L
-
-        with _L._pattern_cache_lock:
-            _L._pattern_cache.clear()
+        _L.clear_upload_caches()
         barrier(dist)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -389,8 +402,9 @@ def run_b200(args, rank, world, dist):
                "d2h_bytes_per_step": int(d2h * world),
                "solve_wall_sum_s": round(sum(r.wall_time for r in reps_e), 3),
                "cold_value": round(t_cold / world, 4),
-               "cold_note": "pattern cache emptied first: the int32 pattern upload and the device SELL view build "
-                            "are inside the timed region (a first call in a fresh process)",
+               "cold_note": "upload caches emptied first: the int32 pattern upload, the device SELL view build and "
+                            "(C3) the upload of the two affine value arrays are inside the timed region (a first "
+                            "call in a fresh process)",
                "path": "run_sequence over host CSR (reference-style SparseSpdMatrix fields); returns numpy solutions"}
 
     ach = alg_bytes / (avg[0] * 1e-3) / 1e9 if avg[0] > 0 else None  # C1: single-CTA batches, no per-kernel samples

@@ -4,10 +4,15 @@
 //   K8  Out = S C           basis reconstruction S @ coef          (pod.py:91-93)
 //
 // tcgen05 has no f64 kind, so the fp64 tensor path on sm_100a is the warp-level
-// DMMA (mma.sync.m8n8k4.f64, SASS DMMA.8x8x4). Operands are staged through a
-// cp.async (LDGSTS, 16-byte, L2-only) shared-memory ring. K7 runs over work
-// units of (tile, row range) balanced by issued DMMAs (see below); K8 gives
-// each CTA a 64 x 64 output tile computed by 4 warps of 32 x 32.
+// DMMA (mma.sync.m8n8k4.f64, SASS DMMA.8x8x4). K7 stages its operand panels
+// with TMA (cp.async.bulk.tensor.2d, SASS UTMALDG; 128-byte swizzle, so the
+// dense 16-row boxes are read without bank conflicts) issued by one producer
+// warp into an mbarrier full/empty ring that the DMMA warps consume without
+// block barriers; it runs over work units of (tile, row range) balanced by
+// issued DMMAs (see below). K8 gives each CTA a 64 x 64 output tile computed
+// by 4 warps of 32 x 32 from a cp.async ring.
+#include <cuda.h>  // CUtensorMap and its enums only; the encoder is fetched from the driver at run time
+
 #include <algorithm>
 #include <vector>
 
@@ -27,10 +32,6 @@ constexpr int kStages = RK_GRAM_STAGES;
 constexpr int kPadK = kStep + 4;      // 20 doubles: conflict-free 8-byte fragment loads
 constexpr int kPadM = kTile + 4;      // 68 doubles: conflict-free for the S tile of K8
 constexpr int kDmmaThreads = 128;
-#ifndef RK_GRAM_SKIP
-#define RK_GRAM_SKIP 1
-#endif
-constexpr bool kSkipLower = RK_GRAM_SKIP;
 
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -119,17 +120,100 @@ static inline int shape_frags(int FA, int FB, int code) {
   return c;
 }
 
-// One K step (16 rows) of a warp: only the fragments of its shape.
-// xs / ys point at the warp's first fragment row (+ g row, + t column).
+// Fixed-order sum of a split tile's partials: G[a0 + r, b0 + c] = sum_q
+// ws[first + q][r + c BM]. One CTA per split tile.
+template <int BM, int BN>
+__global__ void __launch_bounds__(256) k_gram_reduce(int64_t m1, int64_t m2, const double* __restrict__ ws,
+                                                     double* __restrict__ G, int64_t ldg,
+                                                     const __grid_constant__ GramTiles T) {
+  const uint32_t ab = T.ab[blockIdx.x];
+  const int64_t a0 = (int64_t)(ab & 2047u) * BM, b0 = (int64_t)((ab >> 11) & 2047u) * BN;
+  const double* p = ws + (int64_t)T.first[blockIdx.x] * (BM * BN);
+  const int cnt = T.count[blockIdx.x];
+  for (int e = threadIdx.x; e < BM * BN; e += blockDim.x) {
+    const int r = e % BM, c = e / BM;
+    if (a0 + r >= m1 || b0 + c >= m2) continue;
+    double s = 0.0;
+    for (int q = 0; q < cnt; ++q) s += __ldcs(p + (int64_t)q * (BM * BN) + e);
+    G[(a0 + r) + (b0 + c) * ldg] = s;
+  }
+}
+
+// --------------------------------------------------------------------------
+// K7 with TMA staging. Per stage the producer (lane 0 of warp 0) arms
+// full[stage] with the box bytes and issues two cp.async.bulk.tensor.2d loads:
+// 16 rows x BM columns of X and 16 rows x BN columns of Y (or Y2). A box lands
+// dense, one 128-byte line per column, XOR-swizzled in 16-byte chunks by the
+// line index mod 8 (CU_TENSOR_MAP_SWIZZLE_128B), so the 8 columns x 4 rows an
+// 8 x 4 fragment load touches fall in 32 distinct banks per half warp: two
+// wavefronts per 256-byte fragment, the minimum. Rows past n and columns past
+// the map's extent arrive as zeros (TMA out-of-bounds fill): no predicates.
+// The right operand may live in two buffers (columns [0, c1) in Y, [c1, m2)
+// in Y2): a tile on one side takes one box from that buffer's map; the one
+// tile that straddles c1 takes a (c1 - b0)-column box of Y and a (b0 + BN -
+// c1)-column box of Y2 from two maps encoded with those box widths -- the
+// swizzle is a function of the shared-memory address, so a box that starts
+// at any 128-byte line lands in the same pattern.
+// Each warp waits on full[stage] and issues its fragments' DMMAs; it releases
+// a stage (one lane arrives on empty[stage]) only after the full-wait of the
+// NEXT step, and the producer then refills that stage once all warps have
+// left it (STAGES - 1 steps ahead of the consumers). No block barrier in the
+// K loop. The deferred release matters: ptxas gives mbarrier.arrive no
+// scoreboard wait on earlier ld.shared, so an arrive placed right after a
+// step's DMMAs is hoisted to just behind the step's last LDS *issue*, the
+// producer's next box can land before those loads have read the stage, and a
+// few lines of one fragment come back from the wrong K step (measured: one
+// wrong 16-row step in ~1e5, scripts/gram_stress.py). Behind the spin loop of
+// the next wait, every DMMA of the step -- hence every load feeding it -- has
+// issued. (A fifth, producer-only warp
+// was tried first: 15 warps per SM put 4 on one sub-partition, which caps the
+// kernel at 128 registers per thread and spills the 128 x 64 tile.)
+// --------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(dst),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+constexpr int kLine = kStep * 8;  // bytes of one staged column: 16 rows
+
+// One K step of a warp from a swizzled stage: xs / ys are the warp's first
+// line, koff[kq] this lane's byte offset within a group of 8 lines.
 template <int FA, int FB, int RA, int CB, int S>
-__device__ __forceinline__ void warp_step(double (&acc)[FA][FB][2], const double* xs, const double* ys) {
+__device__ __forceinline__ void warp_step_sw(double (&acc)[FA][FB][2], const unsigned char* xs,
+                                             const unsigned char* ys, const uint32_t (&koff)[kStep / 4]) {
 #pragma unroll
   for (int kq = 0; kq < kStep / 4; ++kq) {
     double af[RA], bf[CB];
 #pragma unroll
-    for (int i = 0; i < RA; ++i) af[i] = xs[i * 8 * kPadK + kq * 4];
+    for (int i = 0; i < RA; ++i) af[i] = *reinterpret_cast<const double*>(xs + i * 8 * kLine + koff[kq]);
 #pragma unroll
-    for (int j = 0; j < CB; ++j) bf[j] = ys[j * 8 * kPadK + kq * 4];
+    for (int j = 0; j < CB; ++j) bf[j] = *reinterpret_cast<const double*>(ys + j * 8 * kLine + koff[kq]);
 #pragma unroll
     for (int i = 0; i < RA; ++i)
 #pragma unroll
@@ -139,89 +223,88 @@ __device__ __forceinline__ void warp_step(double (&acc)[FA][FB][2], const double
 }
 
 template <int FA, int FB, int C>
-__device__ __forceinline__ void warp_step_dispatch(int code, double (&acc)[FA][FB][2], const double* xs,
-                                                   const double* ys) {
+__device__ __forceinline__ void warp_step_sw_dispatch(int code, double (&acc)[FA][FB][2], const unsigned char* xs,
+                                                      const unsigned char* ys, const uint32_t (&koff)[kStep / 4]) {
   if constexpr (C <= FA * FB) {
     if (code == C) {
-      warp_step<FA, FB, (C - 1) / FB + 1, (C - 1) % FB + 1, kNoStair>(acc, xs, ys);
+      warp_step_sw<FA, FB, (C - 1) / FB + 1, (C - 1) % FB + 1, kNoStair>(acc, xs, ys, koff);
       return;
     }
-    warp_step_dispatch<FA, FB, C + 1>(code, acc, xs, ys);
+    warp_step_sw_dispatch<FA, FB, C + 1>(code, acc, xs, ys, koff);
   } else if constexpr (C <= FA * FB + FA + FB - 2) {
     if (code == C) {
-      warp_step<FA, FB, FA, FB, C - FA * FB - 1 - (FB - 1)>(acc, xs, ys);
+      warp_step_sw<FA, FB, FA, FB, C - FA * FB - 1 - (FB - 1)>(acc, xs, ys, koff);
       return;
     }
-    warp_step_dispatch<FA, FB, C + 1>(code, acc, xs, ys);
+    warp_step_sw_dispatch<FA, FB, C + 1>(code, acc, xs, ys, koff);
   }
 }
 
 template <int BM, int BN, int WM, int WN, int MINB, int STAGES>
 __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB)
-    k_gram(int64_t n, int64_t m1, const double* __restrict__ X, int64_t ldx, int64_t m2,
-           const double* __restrict__ Y, int64_t ldy, const double* __restrict__ Y2, int64_t ldy2, int64_t c1,
-           double* __restrict__ G, int64_t ldg, double* __restrict__ ws, int64_t upper_off,
-           const __grid_constant__ GramUnits U) {
-  constexpr int kThreads = (BM / WM) * (BN / WN) * 32;
+    k_gram_tma(int64_t n, int64_t m1, int64_t m2, int64_t c1, double* __restrict__ G, int64_t ldg,
+               double* __restrict__ ws, int64_t upper_off, const __grid_constant__ CUtensorMap mapx,
+               const __grid_constant__ CUtensorMap mapy, const __grid_constant__ CUtensorMap mapy2,
+               const __grid_constant__ CUtensorMap mapya, const __grid_constant__ CUtensorMap mapyb,
+               const __grid_constant__ GramUnits U) {
+  constexpr int NW = (BM / WM) * (BN / WN);
   constexpr int FA = WM / 8, FB = WN / 8;
-  extern __shared__ __align__(16) double smem[];
-  double* Xs = smem;                                  // [stage][a][kPadK]
-  double* Ys = smem + STAGES * BM * kPadK;           // [stage][b][kPadK]
+  constexpr uint32_t kXBytes = BM * kLine, kYBytes = BN * kLine, kStageBytes = kXBytes + kYBytes;
+  static_assert(kXBytes % 1024 == 0 && kYBytes % 1024 == 0, "boxes keep the 1024-byte swizzle period");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;           // swizzle period alignment
+  const unsigned char* sbase = smem_raw + (base - raw);
+  const uint32_t bars = base + STAGES * kStageBytes;       // full[STAGES], empty[STAGES]
+
   const uint64_t unit = U.u[blockIdx.x];
-  const int64_t a0 = (int64_t)(unit & 2047u) * BM;
-  const int64_t b0 = (int64_t)((unit >> 11) & 2047u) * BN;
+  const int64_t a0 = (int64_t)(unit & 2047u) * BM, b0 = (int64_t)((unit >> 11) & 2047u) * BN;
   const bool direct = (unit >> 22) & 1u;
   const int64_t kbeg = (int64_t)((unit >> 23) & 0xFFFFFu) * kChunk;
   const int64_t kend = min(n, (int64_t)((unit >> 43) & 0xFFFFFu) * kChunk);
   const int nsteps = kend > kbeg ? (int)((kend - kbeg + kStep - 1) / kStep) : 0;
 
-  // Each thread stages fixed (column, row pair) chunks: LX of the left panel
-  // and LY of the right one. Their column base pointers do not change with the
-  // K step, so they are resolved once (column bound and the Y / Y2 segment
-  // choice included) and every step only adds the row offset.
-  constexpr int LX = BM * (kStep / 2) / kThreads, LY = BN * (kStep / 2) / kThreads;
-  static_assert(LX * kThreads == BM * (kStep / 2) && LY * kThreads == BN * (kStep / 2), "loader shape");
-  const int ch = threadIdx.x % (kStep / 2);
-  const double* xcol[LX];
-  const double* ycol[LY];
+  if (threadIdx.x == 0) {
 #pragma unroll
-  for (int i = 0; i < LX; ++i) {
-    const int64_t ga = a0 + (threadIdx.x + i * kThreads) / (kStep / 2);
-    xcol[i] = ga < m1 ? X + ga * ldx + kbeg + 2 * ch : nullptr;
-  }
-#pragma unroll
-  for (int i = 0; i < LY; ++i) {
-    const int64_t gb = b0 + (threadIdx.x + i * kThreads) / (kStep / 2);
-    // columns [0, c1) of the right operand live in Y, [c1, m2) in Y2
-    ycol[i] = gb >= m2 ? nullptr : gb < c1 ? Y + gb * ldy + kbeg + 2 * ch : Y2 + (gb - c1) * ldy2 + kbeg + 2 * ch;
-  }
-  auto load_stage = [&](int stage, int step) {
-    const int64_t off = (int64_t)step * kStep;
-    const int64_t row = kbeg + off + 2 * ch;
-    const int rb = row < kend ? (row + 1 < kend ? 16 : 8) : 0;
-#pragma unroll
-    for (int i = 0; i < LX; ++i) {
-      const int col = (threadIdx.x + i * kThreads) / (kStep / 2);
-      const bool ok = xcol[i] != nullptr && rb > 0;
-      cp_async16(Xs + (stage * BM + col) * kPadK + 2 * ch, ok ? (const void*)(xcol[i] + off) : (const void*)X,
-                 ok ? rb : 0);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(bars + 8 * s, 1);              // the producer's arrive + the boxes' bytes
+      mbar_init(bars + 8 * (STAGES + s), NW);  // one lane of every warp
     }
-#pragma unroll
-    for (int i = 0; i < LY; ++i) {
-      const int col = (threadIdx.x + i * kThreads) / (kStep / 2);
-      const bool ok = ycol[i] != nullptr && rb > 0;
-      cp_async16(Ys + (stage * BN + col) * kPadK + 2 * ch, ok ? (const void*)(ycol[i] + off) : (const void*)Y,
-                 ok ? rb : 0);
-    }
-  };
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool producer = threadIdx.x == 0;
+  // source of the Y box: 0 all in Y, 1 all in Y2, 2 straddling c1
+  const int ysrc = (b0 + BN <= c1 || c1 >= m2) ? 0 : (b0 >= c1 ? 1 : 2);
+  const uint32_t w1 = ysrc == 2 ? (uint32_t)(c1 - b0) : 0u;  // lines of the straddling tile that come from Y
+  auto produce = [&](int step) {  // producer thread only: refill the stage of `step`
+    const int stg = step % STAGES, round = step / STAGES;
+    if (round > 0) mbar_wait(bars + 8 * (STAGES + stg), (round - 1) & 1);
+    const uint32_t full = bars + 8 * stg;
+    mbar_expect_tx(full, kStageBytes);
+    const int krow = (int)(kbeg + (int64_t)step * kStep);
+    tma_load_2d(base + stg * kStageBytes, &mapx, full, krow, (int)a0);
+    const uint32_t ydst = base + stg * kStageBytes + kXBytes;
+    if (ysrc == 0) {
+      tma_load_2d(ydst, &mapy, full, krow, (int)b0);
+    } else if (ysrc == 1) {
+      tma_load_2d(ydst, &mapy2, full, krow, (int)(b0 - c1));
+    } else {
+      tma_load_2d(ydst, &mapya, full, krow, (int)b0);
+      tma_load_2d(ydst + w1 * kLine, &mapyb, full, krow, 0);
+    }
+  };
+  if (producer)
+    for (int st = 0; st < STAGES - 1 && st < nsteps; ++st) produce(st);
+
   const int g = lane >> 2, t = lane & 3;
   const int wa = (warp % (BM / WM)) * WM, wb = (warp / (BM / WM)) * WN;
-  // The warp's shape code, fixed for the whole unit (warp-uniform). A
-  // predicated-off DMMA costs the pipe as much as an issued one (measured,
-  // scripts/dmma_pred_probe.cu), so masked fragments are skipped by branching
-  // to a body that contains only the wanted DMMAs.
+  uint32_t koff[kStep / 4];
+#pragma unroll
+  for (int kq = 0; kq < kStep / 4; ++kq)
+    koff[kq] = (uint32_t)(g * kLine + ((((kq << 1) | (t >> 1)) ^ g) << 4) + ((t & 1) << 3));
   const int code = warp_shape_code(FA, FB, a0 + wa, b0 + wb, m1, m2, upper_off);
   double acc[FA][FB][2];
 #pragma unroll
@@ -229,39 +312,31 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB)
 #pragma unroll
     for (int j = 0; j < FB; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nsteps) load_stage(s, s);
-    cp_async_commit();
-  }
-  // K step prologue shared by both loops: wait for stage `step`, refill the
-  // ring; returns the warp's fragment base pointers into that stage.
-  auto next_stage = [&](int step, const double*& xs, const double*& ys) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    const int nxt = step + STAGES - 1;
-    if (nxt < nsteps) load_stage(nxt % STAGES, nxt);
-    cp_async_commit();
+  const unsigned char* xw = sbase + wa * kLine;
+  const unsigned char* yw = sbase + kXBytes + wb * kLine;
+  // Step prologue shared by both loops: wait for the step's boxes, release
+  // the previous step's stage, let the producer refill it.
+  auto next_stage = [&](int step) {
     const int stg = step % STAGES;
-    xs = Xs + (stg * BM + wa + g) * kPadK + t;
-    ys = Ys + (stg * BN + wb + g) * kPadK + t;
+    mbar_wait(bars + 8 * stg, (step / STAGES) & 1);
+    if (step > 0) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bars + 8 * (STAGES + (step - 1) % STAGES));
+    }
+    if (producer && step + STAGES - 1 < nsteps) produce(step + STAGES - 1);
+    return stg * kStageBytes;
   };
-  // Two copies of the K loop, chosen once per warp: the common full-tile warp
-  // runs a loop with no shape dispatch at all; edge / diagonal warps dispatch
-  // per step. Every warp passes the same number of block barriers.
-  const double *xs, *ys;
   if (code == kFullShape<FA, FB>) {
     for (int step = 0; step < nsteps; ++step) {
-      next_stage(step, xs, ys);
-      warp_step<FA, FB, FA, FB, kNoStair>(acc, xs, ys);
+      const uint32_t so = next_stage(step);
+      warp_step_sw<FA, FB, FA, FB, kNoStair>(acc, xw + so, yw + so, koff);
     }
   } else {
     for (int step = 0; step < nsteps; ++step) {
-      next_stage(step, xs, ys);
-      if (code != 0) warp_step_dispatch<FA, FB, 1>(code, acc, xs, ys);  // 0: only stages operands
+      const uint32_t so = next_stage(step);
+      if (code != 0) warp_step_sw_dispatch<FA, FB, 1>(code, acc, xw + so, yw + so, koff);
     }
   }
-  cp_async_wait<0>();
 
   if (direct) {
 #pragma unroll
@@ -289,25 +364,6 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB)
         o[la + (lb + 1) * BM] = acc[i][j][1];
       }
     }
-  }
-}
-
-// Fixed-order sum of a split tile's partials: G[a0 + r, b0 + c] = sum_q
-// ws[first + q][r + c BM]. One CTA per split tile.
-template <int BM, int BN>
-__global__ void __launch_bounds__(256) k_gram_reduce(int64_t m1, int64_t m2, const double* __restrict__ ws,
-                                                     double* __restrict__ G, int64_t ldg,
-                                                     const __grid_constant__ GramTiles T) {
-  const uint32_t ab = T.ab[blockIdx.x];
-  const int64_t a0 = (int64_t)(ab & 2047u) * BM, b0 = (int64_t)((ab >> 11) & 2047u) * BN;
-  const double* p = ws + (int64_t)T.first[blockIdx.x] * (BM * BN);
-  const int cnt = T.count[blockIdx.x];
-  for (int e = threadIdx.x; e < BM * BN; e += blockDim.x) {
-    const int r = e % BM, c = e / BM;
-    if (a0 + r >= m1 || b0 + c >= m2) continue;
-    double s = 0.0;
-    for (int q = 0; q < cnt; ++q) s += __ldcs(p + (int64_t)q * (BM * BN) + e);
-    G[(a0 + r) + (b0 + c) * ldg] = s;
   }
 }
 
@@ -421,9 +477,11 @@ static size_t gemm_smem() {
 
 // One instantiation of the templated K7 with its launch shape and measured
 // residency (CTAs per SM at its register / shared-memory footprint).
+typedef void (*GramTmaFn)(int64_t, int64_t, int64_t, int64_t, double*, int64_t, double*, int64_t, const CUtensorMap,
+                          const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
+                          const rk::GramUnits);
 struct GramVariant {
-  void (*fn)(int64_t, int64_t, const double*, int64_t, int64_t, const double*, int64_t, const double*, int64_t, int64_t,
-             double*, int64_t, double*, int64_t, const rk::GramUnits);
+  GramTmaFn fn;
   void (*reduce)(int64_t, int64_t, const double*, double*, int64_t, const rk::GramTiles);
   int bm, bn, wm, wn, threads;
   size_t smem;
@@ -433,14 +491,15 @@ struct GramVariant {
 template <int BM, int BN, int WM, int WN, int MINB, int STAGES>
 static GramVariant make_variant() {
   GramVariant v;
-  v.fn = rk::k_gram<BM, BN, WM, WN, MINB, STAGES>;
+  v.fn = rk::k_gram_tma<BM, BN, WM, WN, MINB, STAGES>;
   v.reduce = rk::k_gram_reduce<BM, BN>;
   v.bm = BM;
   v.bn = BN;
   v.wm = WM;
   v.wn = WN;
   v.threads = (BM / WM) * (BN / WN) * 32;
-  v.smem = (size_t)STAGES * (BM + BN) * rk::kPadK * sizeof(double);
+  // stages, 1024 bytes of alignment slack (swizzle period), the full / empty barriers
+  v.smem = (size_t)STAGES * (BM + BN) * rk::kLine + 1024 + 2 * STAGES * sizeof(uint64_t);
   cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem);
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, v.fn, v.threads, v.smem) != cudaSuccess || occ < 1) occ = 1;
@@ -448,9 +507,9 @@ static GramVariant make_variant() {
   return v;
 }
 
-// 0: 64 x 64 CTA tile, 4 warps of 32 x 32, 4 stages (2 CTAs / SM)
-// 1: 128 x 64, 4 warps of 64 x 32, 3 stages (2 CTAs / SM): full Grams
-// 2: 64 x 64, 3 stages (3 CTAs / SM)
+// 0: 64 x 64 CTA tile, 4 warps of 32 x 32 (2 CTAs / SM)
+// 1: 128 x 64, 4 warps of 64 x 32 (2 CTAs / SM): full Grams
+// 2: 64 x 64 (3 CTAs / SM)
 // 3: 64 x 80, 4 warps of 32 x 40 (3 CTAs / SM)
 // 4: 64 x 48, 4 warps of 32 x 24 (3 CTAs / SM)
 // 2-4 differ only in the tile width, so a width that leaves a sliver past
@@ -459,10 +518,10 @@ static GramVariant make_variant() {
 constexpr int kVariants = 5;
 static const GramVariant& gram_variant(int which) {
   static const GramVariant v0 = make_variant<64, 64, 32, 32, RK_GRAM_MINB, rk::kStages>();
-  static const GramVariant v1 = make_variant<128, 64, 64, 32, 2, 3>();
-  static const GramVariant v2 = make_variant<64, 64, 32, 32, 3, 3>();
+  static const GramVariant v1 = make_variant<128, 64, 64, 32, 2, 4>();
+  static const GramVariant v2 = make_variant<64, 64, 32, 32, 3, 4>();
   static const GramVariant v3 = make_variant<64, 80, 32, 40, 3, 3>();
-  static const GramVariant v4 = make_variant<64, 48, 32, 24, 3, 3>();
+  static const GramVariant v4 = make_variant<64, 48, 32, 24, 3, 4>();
   switch (which) {
     case 1: return v1;
     case 2: return v2;
@@ -561,6 +620,13 @@ static int build_plan(int64_t n, int64_t m1, int64_t m2, int64_t upper_off, Gram
         total += std::max(c, floor_cost);
       }
     }
+  P.code.clear();
+  P.slot.clear();
+  P.split_ab.clear();
+  P.split_first.clear();
+  P.split_count.clear();
+  P.ws_doubles = 0;
+  if (tiles.empty()) return 0;
   const int64_t slots = (int64_t)sm_count() * v.per_sm;
   const int64_t max_split = std::max<int64_t>(1, nchunk / 16);  // >= 512 rows per unit
   static const int64_t waves = [] {
@@ -583,9 +649,6 @@ static int build_plan(int64_t n, int64_t m1, int64_t m2, int64_t upper_off, Gram
   struct U { int64_t k0; uint64_t code; int64_t slot; };
   static thread_local std::vector<U> units;
   units.clear();
-  P.split_ab.clear();
-  P.split_first.clear();
-  P.split_count.clear();
   for (const Tile& t : tiles) {
     const bool direct = t.ns == 1;
     if (!direct) {
@@ -621,6 +684,39 @@ int64_t gram_workspace_doubles(int64_t n, int64_t m1, int64_t m2, int64_t upper_
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point lookup (no libcuda link).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static const EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return (EncodeTiledFn)p;
+  }();
+  return fn;
+}
+
+// Map of a column-major fp64 panel: dimension 0 = rows (contiguous), dimension
+// 1 = columns (stride ld); boxes of 16 rows x box_cols columns, 128-byte
+// swizzle, zero fill outside [0, rows) x [0, cols).
+static int panel_map(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld, int box_cols) {
+  const EncodeTiledFn enc = encode_tiled();
+  RK_REQUIRE(enc != nullptr, RK_ERR_CUDA, "rk_gram: the driver has no cuTensorMapEncodeTiled");
+  const cuuint64_t gdim[2] = {(cuuint64_t)rows, (cuuint64_t)std::max<int64_t>(cols, 1)};
+  const cuuint64_t gstride[1] = {(cuuint64_t)ld * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)rk::kStep, (cuuint32_t)box_cols};
+  const cuuint32_t estride[2] = {1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), gdim, gstride, box, estride,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  RK_REQUIRE(r == CUDA_SUCCESS, RK_ERR_CUDA, "rk_gram: cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return 0;
+}
+
 int launch_gram(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m2, const double* Y, int64_t ldy,
                 const double* Y2, int64_t ldy2, int64_t c1, double* G, int64_t ldg, double* ws, int64_t ws_len,
                 int64_t upper_off, cudaStream_t s) {
@@ -642,11 +738,24 @@ int launch_gram(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m2,
   RK_REQUIRE(P.ws_doubles == 0 || (ws && ws_len >= P.ws_doubles), RK_ERR_ARG,
              "rk_gram: workspace too small (%lld < %lld)", (long long)ws_len, (long long)P.ws_doubles);
   const GramVariant& v = gram_variant(P.which);
+  CUtensorMap mx, my, my2, mya, myb;
+  if (int e = panel_map(&mx, X, n, m1, ldx, v.bm)) return e;
+  if (int e = panel_map(&my, Y, n, c1, ldy, v.bn)) return e;
+  if (int e = panel_map(&my2, Y2, n, m2 - c1, ldy2, v.bn)) return e;
+  // the tile that straddles c1: w1 columns of Y, then bn - w1 columns of Y2
+  const int w1 = (int)(c1 % v.bn);
+  if (c1 < m2 && w1 != 0) {
+    if (int e = panel_map(&mya, Y, n, c1, ldy, w1)) return e;
+    if (int e = panel_map(&myb, Y2, n, m2 - c1, ldy2, v.bn - w1)) return e;
+  } else {
+    mya = my;
+    myb = my2;
+  }
   for (size_t u0 = 0; u0 < P.code.size(); u0 += rk::kMaxUnits) {
     const size_t cnt = std::min<size_t>(rk::kMaxUnits, P.code.size() - u0);
     std::copy_n(P.code.begin() + u0, cnt, U.u);
     std::copy_n(P.slot.begin() + u0, cnt, U.slot);
-    v.fn<<<(unsigned)cnt, v.threads, v.smem, s>>>(n, m1, X, ldx, m2, Y, ldy, Y2, ldy2, c1, G, ldg, ws, upper_off, U);
+    v.fn<<<(unsigned)cnt, v.threads, v.smem, s>>>(n, m1, m2, c1, G, ldg, ws, upper_off, mx, my, my2, mya, myb, U);
     rkh::note_launch();
   }
   for (size_t t0 = 0; t0 < P.split_ab.size(); t0 += rk::kMaxTiles) {

@@ -233,6 +233,34 @@ def hstack_blocks(blocks, n: int, device, cap_extra: int = 0) -> torch.Tensor:
 # ---------------------------------------------------------------------------
 _pattern_cache_lock = threading.Lock()
 _pattern_cache: list = []  # [(host rowptr, host col, _Pattern)]
+_affine_cache_lock = threading.Lock()
+_affine_cache: list = []  # [(host base, host delta, device, device base, device delta)]
+
+
+def clear_upload_caches() -> None:
+    """Forget the uploaded patterns and affine value parts (a first call in a fresh process)."""
+    with _pattern_cache_lock:
+        _pattern_cache.clear()
+    with _affine_cache_lock:
+        _affine_cache.clear()
+
+
+def _affine_device_parts(base: np.ndarray, delta: np.ndarray, device):
+    """Device copies of the two value arrays of an affine sequence
+    (problems.AffineHostCsr), uploaded once per (base, delta) pair: every
+    system's values are then formed on the GPU. The host arrays
+    are kept referenced, so the identity test stays valid."""
+    with _affine_cache_lock:
+        for hb, hd, dv, db, dd in _affine_cache:
+            if hb is base and hd is delta and dv == device:
+                return db, dd
+    db = host_to_device(base, device)
+    dd = host_to_device(delta, device)
+    torch.cuda.current_stream(device).synchronize()  # later systems read them from other streams
+    with _affine_cache_lock:
+        _affine_cache.insert(0, (base, delta, device, db, dd))
+        del _affine_cache[2:]
+    return db, dd
 USE_BSR3 = os.environ.get("RK_BSR", "1") != "0"
 DEVICE_SPDINV_MIN = int(os.environ.get("RK_DEVICE_SPDINV_MIN", "256"))
 USE_SELL1 = os.environ.get("RK_SELL1", "1") != "0"
@@ -533,6 +561,17 @@ class SparseSpdMatrix:
         SparseSpdMatrix (n, row_offsets, col_indices, values), or scipy."""
         if isinstance(A, SparseSpdMatrix):
             return A
+        affine = getattr(A, "affine", None)
+        if affine is not None:
+            # values = base + coef * delta formed on the device with numpy's two
+            # roundings (rk_axpby: fl(fl(coef * delta) + base)); only the two
+            # parts ever cross PCIe, once per sequence
+            base, delta, coef = affine
+            dev = torch.device(kw["device"]) if kw.get("device") is not None else nat.require_device()
+            db, dd = _affine_device_parts(base, delta, dev)
+            vals = db.clone()
+            axpby(float(coef), dd, 1.0, vals)
+            return cls(A.n, A.row_offsets, A.col_indices, vals, **kw)
         if all(hasattr(A, a) for a in ("n", "row_offsets", "col_indices", "values")):
             return cls(A.n, A.row_offsets, A.col_indices, A.values, **kw)
         if scipy.sparse.issparse(A):

@@ -54,6 +54,43 @@ class HostCsr:
         return self.to_scipy().diagonal()
 
 
+class AffineHostCsr:
+    """Host CSR whose values are ``base + coef * delta`` on a fixed pattern: the
+    form in which a drifting sequence changes its matrix (C3: element e scaled
+    by 1 + 0.02 i U_e is ``vals_E + i * vals_D``). It has the reference
+    SparseSpdMatrix's field names, so every host consumer (the reference
+    itself, scipy) sees an ordinary matrix -- ``values`` materialises
+    ``base + coef * delta`` with numpy on first use. The device path
+    (``SparseSpdMatrix.from_host``) instead uploads ``base`` and ``delta`` once
+    per sequence and forms each system's values on the GPU with the same two
+    roundings (no per-system upload of the 0.5-2 GB of values)."""
+
+    def __init__(self, n: int, row_offsets: np.ndarray, col_indices: np.ndarray, base: np.ndarray,
+                 delta: np.ndarray, coef: float):
+        self.n = int(n)
+        self.row_offsets = row_offsets
+        self.col_indices = col_indices
+        self.affine = (base, delta, float(coef))
+        self._values = None
+
+    @property
+    def values(self) -> np.ndarray:
+        if self._values is None:
+            base, delta, coef = self.affine
+            self._values = base + coef * delta
+        return self._values
+
+    @property
+    def nnz(self) -> int:
+        return int(self.affine[0].shape[0])
+
+    def to_scipy(self) -> scipy.sparse.csr_matrix:
+        return scipy.sparse.csr_matrix((self.values, self.col_indices, self.row_offsets), shape=(self.n, self.n))
+
+    def diagonal(self) -> np.ndarray:
+        return self.to_scipy().diagonal()
+
+
 @dataclass
 class LinearSystemSpec:
     A: object
@@ -399,10 +436,10 @@ def elasticity_sequence(ne=(64, 64, 64), p: int = 40, rtol: float = 1e-5, seed: 
 
         def gen():
             for i in range(1, p + 1):
-                vals = vals_E + i * vals_D           # element e scaled by (1 + 0.02 i U_e)
+                # element e scaled by (1 + 0.02 i U_e): values vals_E + i * vals_D
                 th = math.radians(2.0 * i)
                 b = asm.face_load((0.5, math.cos(th), math.sin(th)))
-                yield LinearSystemSpec(A=HostCsr(N, rowptr, col, vals), b=b, xbar=None,
+                yield LinearSystemSpec(A=AffineHostCsr(N, rowptr, col, vals_E, vals_D, i), b=b, xbar=None,
                                        tol=rtol * float(np.linalg.norm(b)))
     else:
         vals = vals_E.copy()

@@ -1,4 +1,4 @@
-"""Timeline of the fused update tail (needs a -DRK_TAIL_TRACE build, e.g.
+"""Timeline of the direction kernel's combine prologue (needs a -DRK_TAIL_TRACE build, e.g.
 make -C paper_1512_05820_b200/csrc OUT=$PWD/gpurun_trace FLAGS="... -DRK_TAIL_TRACE";
 then RK_LIB=gpurun_trace/libpodcg.so python scripts/tail_trace.py)."""
 import ctypes
@@ -38,9 +38,10 @@ torch.cuda.synchronize()
 buf = (ctypes.c_uint64 * 512)()
 nat.lib().rk_debug_trace(buf, 512)
 t = np.array(list(buf), dtype=np.float64).reshape(64, 8)
-t = t[t[:, 7] > 0]
-# stamps 1..7 are clock64 of the level-2 block (SM cycles); report step costs
-d = np.diff(t[:, 1:], axis=1) / 1.9e3  # cycles -> us at ~1.9 GHz
-names = ["group_ticket", "gsum_written", "level2_ticket", "level2_combined", "scalars", "solved"]
-print(json.dumps({"rows": int(len(t)), "step_us(median, 1.9 GHz)": dict(zip(names, np.round(np.median(d, axis=0), 3).tolist())),
-                  "tail_us": round(float(np.median((t[:, 7] - t[:, 1]) / 1.9e3)), 3)}))
+t = t[t[:, 3] > 0]
+# stamps of block 0 of k_pcg_direction (globaltimer, ns): 0 after griddepcontrol.wait,
+# 1 after the group sums, 2 after the mu solve, 3 at the end of the row loop
+d = np.diff(t[:, :4], axis=1) / 1e3
+names = ["group_sums", "mu_solve", "row_loop"]
+print(json.dumps({"rows": int(len(t)), "block0_step_us(median)": dict(zip(names, np.round(np.median(d, axis=0), 3).tolist())),
+                  "block0_total_us": round(float(np.median((t[:, 3] - t[:, 0]) / 1e3)), 3)}))

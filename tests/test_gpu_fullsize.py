@@ -283,11 +283,21 @@ def test_c4_prefix_matches_reference(pk):
     system 2 the stage-1 direct projection onto the 125 stored directions
     followed by augmented CG. The north-star bar on every system: identical
     stage-3 iterations and matvecs, x (at 2000 fixed indices) within 1e-8,
-    q = c'x within 1e-10."""
+    q = c'x within 1e-10 -- or, where the reference does not reproduce itself
+    to that bar, within twice its own run-to-run difference: a second recykl
+    run of system 1 (c4_prefix3.npz, other BLAS thread count) moved q by
+    6.4e-9 and x by 4.9e-9 at identical counters (rtol 1e-6 stops the
+    iteration long before 1e-10, and numpy's dot order follows the threads)."""
     from paper_1512_05820_b200.problems import elasticity_sequence
 
     d = _reference_run("c4_prefix")
+    d2 = _reference_run("c4_prefix3")
     p = int(d["p_done"])
+    p2 = min(int(d2["p_done"]), p)
+    assert d2["iters"][:p2].tolist() == d["iters"][:p2].tolist()
+    env_q = float(np.max(np.abs(d2["q"][:p2] - d["q"][:p2]) / np.abs(d["q"][:p2])))
+    env_x = float(np.max(np.linalg.norm(d2["xs"][:p2] - d["xs"][:p2], axis=1) / np.linalg.norm(d["xs"][:p2], axis=1)))
+    tol_q, tol_x = max(1e-10, 2 * env_q), max(1e-8, 2 * env_x)
     seq = elasticity_sequence((128, 128, 64), p=p, rtol=1e-6, seed=4, dynamic=True)
     cfg = pk.SolverConfig(truncation=pk.TruncationConfig(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0,
                                                          storage_cap=3000, max_dim=60), mode="cg")
@@ -300,8 +310,8 @@ def test_c4_prefix_matches_reference(pk):
     for j, x in enumerate(xs):
         xh = _host(x)
         q = float(seq.C[0] @ xh)
-        assert abs(q - d["q"][j]) <= 1e-10 * abs(d["q"][j]), (j, q, d["q"][j])
-        assert np.linalg.norm(xh[idx] - d["xs"][j]) <= 1e-8 * np.linalg.norm(d["xs"][j]), j
+        assert abs(q - d["q"][j]) <= tol_q * abs(d["q"][j]), (j, q, d["q"][j])
+        assert np.linalg.norm(xh[idx] - d["xs"][j]) <= tol_x * np.linalg.norm(d["xs"][j]), j
 
 
 def test_c5_full_size_matches_reference(pk):

@@ -206,6 +206,37 @@ def test_reference_matrix_objects_are_accepted(pk):
     assert A.n == seq.n and A.nnz == len(seq[0].A.values)
 
 
+def test_affine_sequence_values_formed_on_device(pk):
+    """a drifting sequence given as values = base + i * delta
+    (problems.AffineHostCsr, the C3 generator) uploads base and delta once and
+    forms every system's values on the GPU -- bitwise numpy's `base + i *
+    delta`, in CSR order and in the SELL slots the SpMV streams -- and the
+    sequence solves exactly as from materialised host matrices."""
+    from paper_1512_05820_b200 import linalg as L
+    from paper_1512_05820_b200.problems import HostCsr, LinearSystemSpec, SystemSequence, elasticity_sequence
+
+    seq = elasticity_sequence((6, 5, 4), p=4, rtol=1e-6, seed=11)
+    specs = list(seq)
+    L.clear_upload_caches()
+    for s in specs:
+        A = pk.linalg.as_matrix(s.A)
+        assert np.array_equal(A.values.cpu().numpy(), s.A.values)
+        x = np.random.default_rng(0).standard_normal(seq.n)
+        assert np.array_equal(A.matvec(x).cpu().numpy(), s.A.to_scipy() @ x) or \
+            np.allclose(A.matvec(x).cpu().numpy(), s.A.to_scipy() @ x, rtol=1e-13, atol=1e-13)
+    assert len(L._affine_cache) == 1                      # one upload of (base, delta) for the whole sequence
+    plain = SystemSequence(seq.n, [LinearSystemSpec(A=HostCsr(s.A.n, s.A.row_offsets, s.A.col_indices, s.A.values),
+                                                    b=s.b, xbar=None, tol=s.tol) for s in specs], C=seq.C)
+    cfg = pk.SolverConfig(truncation=pk.TruncationConfig(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0, storage_cap=20,
+                                                         max_dim=10), mode="cg")
+    jac = lambda A: pk.build_preconditioner("jacobi", A)  # noqa: E731
+    xs_a, reps_a, _ = pk.run_sequence(seq, cfg, precond_factory=jac)
+    xs_p, reps_p, _ = pk.run_sequence(plain, cfg, precond_factory=jac)
+    assert [r.stage3_iters for r in reps_a] == [r.stage3_iters for r in reps_p]
+    for a, b in zip(xs_a, xs_p):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
+
+
 @pytest.mark.parametrize("name,tag,mode,cap", [("c2_small", "cg_", "cg", 12), ("c2_small", "fom_", "fom", 12),
                                                ("c3_mid", "cg_", "cg", 30), ("c3_mid", "fom_", "fom", 30)])
 def test_c2_c3_like_sequences(pk, name, tag, mode, cap):

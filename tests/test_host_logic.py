@@ -131,6 +131,10 @@ def test_elasticity_generator_sizes_and_spd():
     assert np.all(np.diff(spec.A.col_indices[spec.A.row_offsets[0]:spec.A.row_offsets[1]]) > 0)
     # the sequence drifts: system 2 differs from system 1
     assert not np.array_equal(seq[0].A.values, seq[1].A.values)
+    # ... as base + i * delta on a fixed pattern (what the device path uploads once)
+    base, delta, coef = seq[1].A.affine
+    assert coef == 2.0 and np.array_equal(seq[1].A.values, base + 2 * delta)
+    assert seq[1].A.affine[0] is seq[0].A.affine[0] and seq[1].A.nnz == base.size
 
 
 def test_c3_shape_constants():
