@@ -620,6 +620,7 @@ __global__ void __launch_bounds__(kSpmvThreads) k_sell1_spmv_pcg(const rk_pcg_pl
 // K2 on the scalar SELL view (blockIdx.y = column tile of CT columns): each
 // slot's value and column are loaded once for CT gathered columns; per column
 // the fma order is the SpMV's, so A X[:, j] is bitwise the SpMV of X[:, j].
+constexpr int kSpmmJ = 4;  // columns whose gathers are issued together in the scalar SELL SpMM
 template <int CT>
 __global__ void __launch_bounds__(kSpmvThreads) k_sell1_spmm(const rk_csr A, int64_t m, const double* __restrict__ X,
                                                             int64_t ldx, double* __restrict__ Y, int64_t ldy) {
@@ -648,16 +649,36 @@ __global__ void __launch_bounds__(kSpmvThreads) k_sell1_spmm(const rk_csr A, int
         c[u] = ok ? ld_stream_s32(col + 32 * (t + u)) : 0;
         v[u] = ok ? ld_stream_f64(val + 32 * (t + u)) : 0.0;
       }
+      if (ncol == CT) {
+        // full tile: no per-column branch, so the gathers of kSpmmJ columns
+        // (kSpmmJ x kSell1U loads) are all in flight before their sums
 #pragma unroll
-      for (int j = 0; j < CT; ++j) {
-        if (j < ncol) {
-          const double* xc = X + (c0 + j) * ldx;
-          double xs[kSell1U];
+        for (int j0 = 0; j0 < CT; j0 += kSpmmJ) {
+          double xs[kSpmmJ][kSell1U];
 #pragma unroll
-          for (int u = 0; u < kSell1U; ++u) xs[u] = __ldg(xc + c[u]);
+          for (int jj = 0; jj < kSpmmJ; ++jj) {
+            const double* xc = X + (c0 + j0 + jj) * ldx;
 #pragma unroll
-          for (int u = 0; u < kSell1U; ++u)
-            if (t + u < width) acc[j] = row_madd(v[u], xs[u], acc[j]);
+            for (int u = 0; u < kSell1U; ++u) xs[jj][u] = __ldg(xc + c[u]);
+          }
+#pragma unroll
+          for (int jj = 0; jj < kSpmmJ; ++jj)
+#pragma unroll
+            for (int u = 0; u < kSell1U; ++u)
+              if (t + u < width) acc[j0 + jj] = row_madd(v[u], xs[jj][u], acc[j0 + jj]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < CT; ++j) {
+          if (j < ncol) {
+            const double* xc = X + (c0 + j) * ldx;
+            double xs[kSell1U];
+#pragma unroll
+            for (int u = 0; u < kSell1U; ++u) xs[u] = __ldg(xc + c[u]);
+#pragma unroll
+            for (int u = 0; u < kSell1U; ++u)
+              if (t + u < width) acc[j] = row_madd(v[u], xs[u], acc[j]);
+          }
         }
       }
     }
@@ -863,16 +884,47 @@ void launch_curvature(const rk_pcg_plan& P, cudaStream_t s) {
   launch_pdl(rk::k_curvature, dim3(curvature_grid(P.n)), dim3(256), 0, s, P);
 }
 
-template <int L>
-static void launch_spmm_l(const rk_csr& A, int64_t m, const double* X, int64_t ldx, double* Y,
-                          int64_t ldy, cudaStream_t s) {
-  constexpr int CT = 8;
+// Columns per pass of the CSR / scalar-SELL SpMM (RK_SPMM_CT = 8, 16 or 32):
+// the matrix is streamed once per pass, so wider passes cut its share of the
+// traffic (C5, 7 nonzeros per row: 84 + 16 CT bytes per row and pass).
+static int spmm_ct() {
+  static const int v = [] {
+    const char* e = getenv("RK_SPMM_CT");
+    const int c = e ? atoi(e) : 8;
+    return (c == 16 || c == 32) ? c : 8;
+  }();
+  return v;
+}
+
+template <int L, int CT>
+static void launch_spmm_lc(const rk_csr& A, int64_t m, const double* X, int64_t ldx, double* Y,
+                           int64_t ldy, cudaStream_t s) {
   const int64_t tiles = (m + CT - 1) / CT;
   const int64_t rpb = rk::kSpmvThreads / L;
   int64_t gx = (A.n + rpb - 1) / rpb;
   gx = std::max<int64_t>(1, std::min<int64_t>(gx, std::max<int64_t>(1, (int64_t)sm_count() * 8 / std::max<int64_t>(1, std::min<int64_t>(tiles, 8)))));
   dim3 grid((unsigned)gx, (unsigned)tiles);
   rk::k_spmm<L, CT><<<grid, rk::kSpmvThreads, 0, s>>>(A.n, A.rowptr, A.col, A.val, m, X, ldx, Y, ldy); rkh::note_launch();
+}
+
+template <int L>
+static void launch_spmm_l(const rk_csr& A, int64_t m, const double* X, int64_t ldx, double* Y,
+                          int64_t ldy, cudaStream_t s) {
+  switch (spmm_ct()) {
+    case 16: launch_spmm_lc<L, 16>(A, m, X, ldx, Y, ldy, s); break;
+    case 32: launch_spmm_lc<L, 32>(A, m, X, ldx, Y, ldy, s); break;
+    default: launch_spmm_lc<L, 8>(A, m, X, ldx, Y, ldy, s); break;
+  }
+}
+
+template <int CT>
+static void launch_sell1_spmm(const rk_csr& A, int64_t m, const double* X, int64_t ldx, double* Y, int64_t ldy,
+                              cudaStream_t s) {
+  const int64_t tiles = (m + CT - 1) / CT;
+  const int64_t need = ((A.n + 31) / 32 + rk::kSpmvThreads / 32 - 1) / (rk::kSpmvThreads / 32);
+  const int64_t gy = std::max<int64_t>(1, std::min<int64_t>(need, 65535));
+  rk::k_sell1_spmm<CT><<<dim3((unsigned)tiles, (unsigned)gy), rk::kSpmvThreads, 0, s>>>(A, m, X, ldx, Y, ldy);
+  note_launch();
 }
 
 template <int CT>
@@ -906,14 +958,11 @@ int launch_spmm(const rk_csr& A, int64_t m, const double* X, int64_t ldx, double
     return e && atoi(e) == 1;
   }();
   if (A.bval && A.bdim == 1 && sell1_spmm) {
-    constexpr int CT = 8;
-    static const int cap = resident_blocks((const void*)rk::k_sell1_spmm<CT>, rk::kSpmvThreads);
-    const int64_t tiles = (m + CT - 1) / CT;
-    const int64_t need = ((A.n + 31) / 32 + rk::kSpmvThreads / 32 - 1) / (rk::kSpmvThreads / 32);
-    (void)cap;
-    const int64_t gy = std::max<int64_t>(1, std::min<int64_t>(need, 65535));
-    rk::k_sell1_spmm<CT><<<dim3((unsigned)tiles, (unsigned)gy), rk::kSpmvThreads, 0, s>>>(A, m, X, ldx, Y, ldy);
-    note_launch();
+    switch (spmm_ct()) {
+      case 16: launch_sell1_spmm<16>(A, m, X, ldx, Y, ldy, s); break;
+      case 32: launch_sell1_spmm<32>(A, m, X, ldx, Y, ldy, s); break;
+      default: launch_sell1_spmm<8>(A, m, X, ldx, Y, ldy, s); break;
+    }
     return cuda_check("rk_spmm (sell1)");
   }
   if (A.bval && A.bdim != 1) {

@@ -25,7 +25,7 @@ def main(path, out, cmd):
         agg[name][0] += 1
         agg[name][1] += us
     total = sum(v[1] for v in agg.values())
-    lines = ["# ncu launch list summary (round 1, after the Gram loader / SELL-1 / wide-mu changes)", "",
+    lines = ["# ncu launch list summary", "",
              f"Command: `{cmd}`", "",
              "Times are cold-cache and serialised (ncu): compare shares, not absolutes.", "",
              f"Total launches: {len(rows)}; listed device time {total / 1e3:.1f} ms", "",

@@ -161,14 +161,19 @@ def test_c2_full_size_prefix_matches_oracle(pk):
 def test_c3_sequence_within_reference_envelope(pk):
     """The bench's 40-system C3 sequence against the reference's own run of it
     (tests/golden/c3_seq.npz, oracle/run_reference_c3.py) and the reference's
-    rounding envelope on its first 18 systems (c3_seq_pert.npz: every RHS
-    scaled by 1 + 1e-15). The reference is chaotic at this size: the 1e-15
-    perturbation moves system 4 by 6 iterations, system 9 by 26 and system 18
-    by 44 (7.3%), q = c'x by up to 6.2e-7 and x by 8.5e-7. So: systems 1-3
-    (reference swing <= 2) within +-2; every system the envelope covers within
-    twice the reference's own relative swing so far plus 1%, with q and x
-    within 5x its envelope; the 40-system iteration total within 5% of the
-    reference's (measured: 23,524 vs 22,513)."""
+    rounding envelope: recykl's own runs of the same sequence with every
+    right-hand side scaled by 1 + 1e-15 and by 1 - 1e-15
+    (c3_seq_pert*.npz, oracle/run_reference_seq.py --pert; the 40-system runs
+    take 100 minutes each, shorter earlier ones are used where they reach).
+    The reference is chaotic at this size in CG mode: a 1e-15 perturbation
+    moves system 4 by 6 iterations, system 9 by 26 and system 18 by 44 (7.3%),
+    q = c'x by up to 6.2e-7 and x by 8.5e-7. So, per system: systems 1-3
+    (reference swing <= 2) within +-2; every system within twice the largest
+    relative swing any perturbed reference run has shown up to that system,
+    plus 1%; q and x within 5x the reference's own envelope on the systems a
+    perturbed run covers; and the 40-system iteration total within 5% of the
+    reference's. (FOM mode, recykl's default, is not chaotic and is held to
+    the plain north-star bar in test_c3_fom_matches_reference_full_size.)"""
     import os
     import warnings
 
@@ -176,14 +181,24 @@ def test_c3_sequence_within_reference_envelope(pk):
 
     gdir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
     d = np.load(os.path.join(gdir, "c3_seq.npz"))
-    e = np.load(os.path.join(gdir, "c3_seq_pert.npz"))
     p = int(d["p_done"])
-    pe = min(int(e["p_done"]), p)
-    ref = d["iters"][:p]
-    env_rel = np.maximum.accumulate(np.abs(e["iters"][:pe] - ref[:pe]) / ref[:pe])
-    env_q = float(np.max(np.abs(e["q"][:pe] - d["q"][:pe]) / np.abs(d["q"][:pe])))
-    env_x = float(np.max(np.linalg.norm(e["xs"][:pe] - d["xs"][:pe], axis=1)
-                         / np.linalg.norm(d["xs"][:pe], axis=1)))
+    ref = d["iters"][:p].astype(float)
+    swing = np.zeros(p)          # largest relative swing of any perturbed run, per system
+    covered = np.zeros(p, bool)
+    env_q = env_x = 0.0
+    for name in ("c3_seq_pert", "c3_seq_pert_m", "c3_seq_pert_p", "c3_seq_pert_m40", "c3_seq_pert_p40"):
+        path = os.path.join(gdir, name + ".npz")
+        if not os.path.exists(path):
+            continue
+        e = np.load(path)
+        pe = min(int(e["p_done"]), p)
+        swing[:pe] = np.maximum(swing[:pe], np.abs(e["iters"][:pe] - ref[:pe]) / ref[:pe])
+        covered[:pe] = True
+        env_q = max(env_q, float(np.max(np.abs(e["q"][:pe] - d["q"][:pe]) / np.abs(d["q"][:pe]))))
+        env_x = max(env_x, float(np.max(np.linalg.norm(e["xs"][:pe] - d["xs"][:pe], axis=1)
+                                        / np.linalg.norm(d["xs"][:pe], axis=1))))
+    env_rel = np.maximum.accumulate(swing)
+    assert covered[:18].all()
     seq = elasticity_sequence((64, 64, 64), p=p, rtol=1e-5, seed=3)
     cfg = pk.SolverConfig(truncation=pk.TruncationConfig(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0,
                                                          storage_cap=60, max_dim=60), mode="cg")
@@ -193,10 +208,13 @@ def test_c3_sequence_within_reference_envelope(pk):
     its = np.array([r.stage3_iters for r in reps])
     assert all(r.converged for r in reps)
     assert np.abs(its[:3] - ref[:3]).max() <= 2
-    assert np.all(np.abs(its[:pe] - ref[:pe]) / ref[:pe] <= 2 * env_rel + 0.01)
+    pc = int(covered.sum())      # perturbed runs cover a prefix
+    assert covered[:pc].all()
+    rel = np.abs(its[:pc] - ref[:pc]) / ref[:pc]
+    assert np.all(rel <= 2 * env_rel[:pc] + 0.01), (rel, env_rel)
     assert abs(int(its.sum()) - int(ref.sum())) <= 0.05 * int(ref.sum())
     idx = d["idx"]
-    for j in range(pe):
+    for j in range(pc):
         xh = _host(xs[j])
         q = float(seq.C[0] @ xh)
         assert abs(q - d["q"][j]) / abs(d["q"][j]) <= max(1e-10, 5 * env_q)

@@ -178,14 +178,17 @@ def test_dmma_gram_shapes(pk, n, m1, m2):
 
 
 @pytest.mark.parametrize("n,m,y_old", [(5000, 7, 3), (3001, 130, 60), (20011, 386, 40), (9000, 700, 60),
-                                       (40000, 129, 0), (1200, 257, 256)])
+                                       (40000, 129, 0), (1200, 257, 256), (700, 130, 60), (513, 64, 0),
+                                       (100, 200, 64), (70000, 640, 64)])
 @pytest.mark.parametrize("single", [True, False])
 def test_dmma_symmetric_gram_upper_shapes(pk, n, m, y_old, single):
     """K7 in upper mode over balanced, fragment-masked units: widths that are
     not tile multiples (386 = 3 x 128 + 2), the two-segment right operand
-    (stage-1 A W + the run's A p_k) and the per-block col_off path; every
-    entry of the upper triangle matches numpy, and repeated calls are
-    bitwise identical (fixed-order split reduction)."""
+    (stage-1 A W + the run's A p_k, one TMA box per buffer and a two-box
+    straddling tile) and the per-block col_off path, diagonal tiles split by
+    fragment-row pairs, few rows (tiles written straight to G) and many
+    (split-K partials); every entry of the upper triangle matches numpy, and
+    repeated calls are bitwise identical (fixed-order split reduction)."""
     from paper_1512_05820_b200.linalg import as_block, symmetric_gram_from_products
 
     rng = np.random.default_rng(n + m)
