@@ -135,6 +135,21 @@ typedef struct rk_pcg_plan {
                              * symmetric); 0: L holds L^{-1} (lower triangular) */
 } rk_pcg_plan;
 
+/* SSOR preconditioner state for a device-stepped PCG run (rk_pcg_*_ssor): the
+ * arguments of rk_ssor_apply. Every application inside a call uses the next
+ * epoch after `epoch`; the caller advances `epoch` by the applications made
+ * (1 for the entry, nsteps for a batch of steps). */
+typedef struct rk_ssor_plan {
+  const double* dw;    /* fl(diag / omega) */
+  const double* d;     /* diag(A) */
+  double* work;        /* n doubles */
+  int32_t* flags;      /* 2n, zero-initialised once */
+  uint32_t* counters;  /* 2 */
+  const int32_t* order_fwd; /* rows of the forward / backward sweep by dependency */
+  const int32_t* order_bwd; /* level (rk_ssor_levels, sorted); NULL = natural order */
+  int32_t epoch;       /* last epoch used */
+} rk_ssor_plan;
+
 const char* rk_last_error(void);
 int rk_device_sm_count(void);
 
@@ -154,6 +169,14 @@ int rk_pcg_entry(const rk_pcg_plan* plan, void* stream);
 /* nsteps full iterations for a CSR operator (K1,K3,K4,K5 per step); steps after
  * convergence/breakdown are no-ops, so the host may overshoot. */
 int rk_pcg_steps(const rk_pcg_plan* plan, int32_t nsteps, int64_t kmax_hint, void* stream);
+/* The same with z = M^{-1} r applied by the SSOR sweeps over plan->A
+ * (preconditioners.py:64-90) instead of the fused Jacobi scaling (plan->dinv is
+ * ignored): per step SpMV, update of x and r (+ ||r||^2), forward and backward
+ * sweep, r'z and cross'z, direction -- all from the device state, no host
+ * synchronisation inside a batch (krylov.py:294-340 with M = SSOR). */
+int rk_pcg_entry_ssor(const rk_pcg_plan* plan, const rk_ssor_plan* ssor, void* stream);
+int rk_pcg_steps_ssor(const rk_pcg_plan* plan, const rk_ssor_plan* ssor, int32_t nsteps, int64_t kmax_hint,
+                      void* stream);
 /* Persistent single-cluster solver for small systems (pcg_cluster.cu): ONE
  * thread-block cluster of <= 16 CTAs runs the iterations of rk_pcg_steps
  * (same statements, cg / fom / paper beta) from st->k until convergence,
@@ -187,9 +210,18 @@ int rk_csr_diagonal(const rk_csr* A, double* diag, double* dinv, int64_t* bad_ro
  * (n doubles), then the backward sweep over its upper triangle with rhs work * d.
  * dw = fl(d / w), d = diag(A). Sync-free triangular solves: flags (2n int32,
  * zero-initialised once) are compared against epoch, which the caller increases
- * with every application; counters: 2 uint32 (reset by the call). */
+ * with every application; counters: 2 uint32 (reset by the call). order_fwd /
+ * order_bwd (n int32 each, or NULL for the natural order): the rows of each
+ * sweep sorted by dependency level, so whole levels are in flight together;
+ * the result does not depend on them. */
 int rk_ssor_apply(const rk_csr* A, const double* dw, const double* d, const double* r, double* z, double* work,
-                  int32_t* flags, uint32_t* counters, int32_t epoch, void* stream);
+                  int32_t* flags, uint32_t* counters, int32_t epoch, const int32_t* order_fwd,
+                  const int32_t* order_bwd, void* stream);
+/* levels[i] = 1 + max levels[j] over row i's strictly lower (upper != 0: strictly
+ * upper) entries: the dependency depth of row i in the forward (backward)
+ * sweep. flags: n int32 compared against epoch as in rk_ssor_apply. */
+int rk_ssor_levels(const rk_csr* A, int32_t upper, int32_t* levels, int32_t* flags, uint32_t* counter,
+                   int32_t epoch, void* stream);
 /* bval[s] = perm[s] >= 0 ? val[perm[s]] : 0 for s < 9*nblk: refresh the
  * 3x3-block slot values of a matrix whose pattern (and perm) was built once
  * for the sequence. */

@@ -60,6 +60,19 @@ class RkPcgState(ctypes.Structure):
     ]
 
 
+class RkSsorPlan(ctypes.Structure):
+    _fields_ = [
+        ("dw", c_vp),
+        ("d", c_vp),
+        ("work", c_vp),
+        ("flags", c_vp),
+        ("counters", c_vp),
+        ("order_fwd", c_vp),
+        ("order_bwd", c_vp),
+        ("epoch", c_i32),
+    ]
+
+
 class RkPcgPlan(ctypes.Structure):
     _fields_ = [
         ("n", c_i64),
@@ -110,6 +123,8 @@ _SIGNATURES = {
     "rk_gram_upper_workspace_doubles": (c_i64, [c_i64, c_i64, c_i64, c_i64]),
     "rk_pcg_entry": (c_i32, [ctypes.POINTER(RkPcgPlan), c_vp]),
     "rk_pcg_steps": (c_i32, [ctypes.POINTER(RkPcgPlan), c_i32, c_i64, c_vp]),
+    "rk_pcg_entry_ssor": (c_i32, [ctypes.POINTER(RkPcgPlan), ctypes.POINTER(RkSsorPlan), c_vp]),
+    "rk_pcg_steps_ssor": (c_i32, [ctypes.POINTER(RkPcgPlan), ctypes.POINTER(RkSsorPlan), c_i32, c_i64, c_vp]),
     "rk_pcg_cluster_eligible": (c_i32, [ctypes.POINTER(RkPcgPlan)]),
     "rk_pcg_cluster_max_rows": (c_i64, []),
     "rk_pcg_run_cluster": (c_i32, [ctypes.POINTER(RkPcgPlan), c_i64, c_vp]),
@@ -141,7 +156,9 @@ _SIGNATURES = {
     "rk_profile_begin": (c_i32, []),
     "rk_launch_count": (c_i64, []),
     "rk_debug_trace": (c_i32, [ctypes.POINTER(ctypes.c_uint64), c_i64]),
-    "rk_ssor_apply": (c_i32, [ctypes.POINTER(RkCsr), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp]),
+    "rk_ssor_apply": (c_i32, [ctypes.POINTER(RkCsr), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp,
+                              c_vp]),
+    "rk_ssor_levels": (c_i32, [ctypes.POINTER(RkCsr), c_i32, c_vp, c_vp, c_vp, c_i32, c_vp]),
     "rk_profile_end": (c_i32, [ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64)]),
     "rk_profile_cluster": (c_i32, [ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64)]),
 }

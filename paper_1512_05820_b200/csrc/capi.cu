@@ -93,7 +93,12 @@ int launch_spmm(const rk_csr& A, int64_t m, const double* X, int64_t ldx, double
 int launch_csr_diagonal(const rk_csr& A, double* diag, double* dinv, int64_t* bad, cudaStream_t s);
 int launch_csr_asymmetry(const rk_csr& A, double* out2, double* ws, int64_t ws_len, uint32_t* tickets, cudaStream_t s);
 int launch_ssor_apply(const rk_csr& A, const double* dw, const double* d, const double* r, double* z, double* u,
-                      int* flags, unsigned int* counters, int epoch, cudaStream_t s);
+                      int* flags, unsigned int* counters, int epoch, cudaStream_t s, const rk_pcg_state* st,
+                      const double* r_even, const int32_t* order_fwd, const int32_t* order_bwd);
+int launch_ssor_levels(const rk_csr& A, int upper, int32_t* lvl, int* flags, unsigned int* counter, int epoch,
+                       cudaStream_t s);
+int pcg_entry_ssor(const rk_pcg_plan& P, const rk_ssor_plan& S, cudaStream_t s);
+int pcg_steps_ssor(const rk_pcg_plan& P, const rk_ssor_plan& S, int nsteps, int64_t kmax_hint, cudaStream_t s);
 int pcg_entry(const rk_pcg_plan& P, cudaStream_t s);
 int pcg_steps(const rk_pcg_plan& P, int nsteps, int64_t kmax_hint, cudaStream_t s);
 int pcg_cluster_eligible(const rk_pcg_plan& P);
@@ -188,6 +193,25 @@ int rk_pcg_steps(const rk_pcg_plan* plan, int32_t nsteps, int64_t kmax_hint, voi
   return rkh::pcg_steps(*plan, nsteps, kmax_hint, as_stream(stream));
 }
 
+static int check_ssor(const rk_pcg_plan* plan, const rk_ssor_plan* S, const char* who) {
+  RK_REQUIRE(plan && S, RK_ERR_ARG, "%s: null plan", who);
+  if (int e = rkh::check_csr(&plan->A)) return e;
+  RK_REQUIRE(plan->A.rowptr && plan->A.col && plan->A.val, RK_ERR_ARG, "%s: CSR operator required", who);
+  RK_REQUIRE(S->dw && S->d && S->work && S->flags && S->counters && S->epoch >= 0, RK_ERR_ARG, "%s: bad SSOR state", who);
+  return RK_OK;
+}
+
+int rk_pcg_entry_ssor(const rk_pcg_plan* plan, const rk_ssor_plan* ssor, void* stream) {
+  if (int e = check_ssor(plan, ssor, "rk_pcg_entry_ssor")) return e;
+  return rkh::pcg_entry_ssor(*plan, *ssor, as_stream(stream));
+}
+
+int rk_pcg_steps_ssor(const rk_pcg_plan* plan, const rk_ssor_plan* ssor, int32_t nsteps, int64_t kmax_hint,
+                      void* stream) {
+  if (int e = check_ssor(plan, ssor, "rk_pcg_steps_ssor")) return e;
+  return rkh::pcg_steps_ssor(*plan, *ssor, nsteps, kmax_hint, as_stream(stream));
+}
+
 int rk_pcg_cluster_eligible(const rk_pcg_plan* plan) { return plan ? rkh::pcg_cluster_eligible(*plan) : 0; }
 
 int64_t rk_pcg_cluster_max_rows(void) { return rkh::pcg_cluster_max_rows(); }
@@ -237,12 +261,23 @@ int rk_csr_diagonal(const rk_csr* A, double* diag, double* dinv, int64_t* bad_ro
 }
 
 int rk_ssor_apply(const rk_csr* A, const double* dw, const double* d, const double* r, double* z, double* work,
-                  int32_t* flags, uint32_t* counters, int32_t epoch, void* stream) {
+                  int32_t* flags, uint32_t* counters, int32_t epoch, const int32_t* order_fwd,
+                  const int32_t* order_bwd, void* stream) {
   if (int e = rkh::check_csr(A)) return e;
   RK_REQUIRE(A->n == 0 || (dw && d && r && z && work && flags && counters), RK_ERR_ARG, "rk_ssor_apply: null pointer");
   RK_REQUIRE(epoch > 0, RK_ERR_ARG, "rk_ssor_apply: epoch must be positive");
   return rkh::launch_ssor_apply(*A, dw, d, r, z, work, reinterpret_cast<int*>(flags),
-                                reinterpret_cast<unsigned int*>(counters), epoch, as_stream(stream));
+                                reinterpret_cast<unsigned int*>(counters), epoch, as_stream(stream), nullptr, nullptr,
+                                order_fwd, order_bwd);
+}
+
+int rk_ssor_levels(const rk_csr* A, int32_t upper, int32_t* levels, int32_t* flags, uint32_t* counter, int32_t epoch,
+                   void* stream) {
+  if (int e = rkh::check_csr(A)) return e;
+  RK_REQUIRE(A->n == 0 || (levels && flags && counter), RK_ERR_ARG, "rk_ssor_levels: null pointer");
+  RK_REQUIRE(epoch > 0, RK_ERR_ARG, "rk_ssor_levels: epoch must be positive");
+  return rkh::launch_ssor_levels(*A, upper, levels, reinterpret_cast<int*>(flags),
+                                 reinterpret_cast<unsigned int*>(counter), epoch, as_stream(stream));
 }
 
 int rk_bsr3_gather(int64_t nblk, const int32_t* perm, const double* val, double* bval, void* stream) {

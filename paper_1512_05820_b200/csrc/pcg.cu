@@ -218,7 +218,13 @@ __device__ __forceinline__ double* r_out(const rk_pcg_plan& P, int64_t k) { retu
 // also writes x, r_{k+1}, z and the ||r||^2, r'z partials. Then each warp
 // reduces 4 columns of cross' z over the chunk (lanes over rows, 16-byte
 // loads, 16 in flight per lane). Partials: part[v * nchunks + chunk].
-__global__ void __launch_bounds__(kUpdThreads, 4) k_pcg_update(const rk_pcg_plan P, int entry, int fused, int64_t group) {
+//
+// ext (a preconditioner applied by its own kernels between two launches,
+// SSOR): 1 = first half, column group 0 only: x, r_{k+1} and the ||r||^2
+// partials, z untouched; 2 = second half: z = M^{-1} r_{k+1} is read from P.z,
+// r'z and the cross'z partials follow. 0 = the fused Jacobi / identity form.
+__global__ void __launch_bounds__(kUpdThreads, 4) k_pcg_update(const rk_pcg_plan P, int entry, int fused, int64_t group,
+                                                               int ext) {
   rk_pcg_state* st = P.st;
   pdl_wait();
   pdl_trigger();
@@ -235,11 +241,14 @@ __global__ void __launch_bounds__(kUpdThreads, 4) k_pcg_update(const rk_pcg_plan
   const bool lead = blockIdx.y == 0;
   const double* __restrict__ p = P.V + k * P.ldv + beg;
   const double* __restrict__ Ap = P.AV + (P.ldav ? k * P.ldav : 0) + beg;
-  const double* __restrict__ rin = r_in(P, k, entry) + beg;
+  const bool second = ext == 2;   // r_{k+1} and x are already updated; z comes from P.z
+  const bool step = !entry && !second;
+  // the residual this launch starts from: r_k, or (second half) the updated r_{k+1}
+  const double* __restrict__ rin = ((second && !entry) ? r_out(P, k) : r_in(P, k, entry)) + beg;
   double* __restrict__ rout = r_out(P, k) + beg;
   double* __restrict__ x = P.x + beg;
   double* __restrict__ z = P.z + beg;
-  const double* __restrict__ dinv = P.dinv ? P.dinv + beg : nullptr;
+  const double* __restrict__ dinv = (P.dinv && ext == 0) ? P.dinv + beg : nullptr;
   double acc[2] = {0.0, 0.0};
   constexpr int R = kProjChunk / kUpdThreads;
   double rv[R], av[R], dv[R], xv[R], pv[R];
@@ -248,10 +257,10 @@ __global__ void __launch_bounds__(kUpdThreads, 4) k_pcg_update(const rk_pcg_plan
     const int i = u * kUpdThreads + threadIdx.x;
     const bool ok = i < rows;
     rv[u] = ok ? rin[i] : 0.0;
-    dv[u] = (ok && dinv) ? __ldg(dinv + i) : 1.0;
-    av[u] = (ok && !entry) ? Ap[i] : 0.0;
-    xv[u] = (ok && !entry && lead) ? x[i] : 0.0;
-    pv[u] = (ok && !entry && lead) ? p[i] : 0.0;
+    dv[u] = (ok && dinv) ? __ldg(dinv + i) : (ok && second) ? z[i] : 1.0;  // second half: dv carries z
+    av[u] = (ok && step) ? Ap[i] : 0.0;
+    xv[u] = (ok && step && lead) ? x[i] : 0.0;
+    pv[u] = (ok && step && lead) ? p[i] : 0.0;
   }
 #pragma unroll
   for (int u = 0; u < R; ++u) {
@@ -261,15 +270,15 @@ __global__ void __launch_bounds__(kUpdThreads, 4) k_pcg_update(const rk_pcg_plan
       continue;
     }
     double ri = rv[u];
-    if (!entry) ri = __dsub_rn(ri, __dmul_rn(alpha, av[u]));     // krylov.py:307
-    const double zi = dinv ? __dmul_rn(ri, dv[u]) : ri;          // preconditioners.py:61
+    if (step) ri = __dsub_rn(ri, __dmul_rn(alpha, av[u]));       // krylov.py:307
+    const double zi = second ? dv[u] : dinv ? __dmul_rn(ri, dv[u]) : ri;  // preconditioners.py:61
     zs[i] = zi;
     if (lead) {
-      if (!entry) {
+      if (step) {
         x[i] = __dadd_rn(xv[u], __dmul_rn(alpha, pv[u]));          // krylov.py:306
         rout[i] = ri;
       }
-      z[i] = zi;
+      if (ext == 0) z[i] = zi;
       acc[0] = fma(ri, ri, acc[0]);
       acc[1] = fma(ri, zi, acc[1]);
     }
@@ -278,12 +287,13 @@ __global__ void __launch_bounds__(kUpdThreads, 4) k_pcg_update(const rk_pcg_plan
   if (lead) {
     block_sum<2>(acc, scratch);  // includes the barrier that publishes zs
     if (threadIdx.x == 0) {
-      part[0 * nchunks + chunk] = acc[0];
-      part[1 * nchunks + chunk] = acc[1];
+      if (ext != 2) part[0 * nchunks + chunk] = acc[0];
+      if (ext != 1) part[1 * nchunks + chunk] = acc[1];
     }
   } else {
     __syncthreads();
   }
+  if (ext == 1) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool vec = ((P.ldc & 1) == 0) && ((((uintptr_t)P.cross) | (beg * 8)) & 15) == 0;
 #pragma unroll 1
@@ -594,13 +604,14 @@ static int64_t fuse_group(int64_t nch) { return std::max<int64_t>(32, (nch + rk:
 // reads the convergence state right after it.
 static bool deferred_combine(const rk_pcg_plan& P) { return P.m <= rk::kFuseMax; }
 
-static void launch_update(const rk_pcg_plan& P, int entry, bool defer, cudaStream_t s, bool mark = false) {
+static void launch_update(const rk_pcg_plan& P, int entry, bool defer, cudaStream_t s, bool mark = false,
+                          int ext = 0) {
   const int64_t nch = update_chunks(P.n);
   const int64_t groups = std::max<int64_t>(1, (P.m + rk::kProjCols - 1) / rk::kProjCols);
-  dim3 grid((unsigned)nch, (unsigned)groups);
-  launch_pdl(rk::k_pcg_update, grid, dim3(rk::kUpdThreads), 0, s, P, entry, defer ? 1 : 0, fuse_group(nch));
+  dim3 grid((unsigned)nch, (unsigned)(ext == 1 ? 1 : groups));
+  launch_pdl(rk::k_pcg_update, grid, dim3(rk::kUpdThreads), 0, s, P, entry, defer ? 1 : 0, fuse_group(nch), ext);
   if (mark) prof_mark(2, s);
-  if (defer) return;
+  if (defer || ext == 1) return;
   const unsigned fgrid = (unsigned)std::min<int64_t>(2 + P.m, 4096);
   const int wide = (P.linv_full && P.wchol > rk::kWideSolve) ? 1 : 0;
   launch_pdl(rk::k_pcg_finish, dim3(fgrid), dim3(256), finish_smem(P.m, wide ? 0 : P.wchol, wide), s, P, entry, nch,
@@ -671,6 +682,48 @@ int pcg_steps(const rk_pcg_plan& P, int nsteps, int64_t kmax_hint, cudaStream_t 
     if (mark) prof_mark(4, s);
   }
   return cuda_check("rk_pcg_steps");
+}
+
+// Device-stepped PCG with the SSOR sweeps between the two halves of the update
+// (rk_pcg_entry_ssor / rk_pcg_steps_ssor). The sweeps are ordinary launches:
+// they start when the first half has completed and the second half (launched
+// with programmatic serialisation) starts when they have.
+int launch_ssor_apply(const rk_csr& A, const double* dw, const double* d, const double* r, double* z, double* u,
+                      int* flags, unsigned int* counters, int epoch, cudaStream_t s, const rk_pcg_state* st,
+                      const double* r_even, const int32_t* order_fwd, const int32_t* order_bwd);
+
+int pcg_entry_ssor(const rk_pcg_plan& P, const rk_ssor_plan& S, cudaStream_t s) {
+  configure_once();
+  if (int e = check_plan(P, true)) return e;
+  const bool defer = deferred_combine(P);
+  launch_update(P, 1, defer, s, false, 1);
+  if (int e = launch_ssor_apply(P.A, S.dw, S.d, P.r, P.z, S.work, reinterpret_cast<int*>(S.flags), S.counters,
+                                S.epoch + 1, s, nullptr, nullptr, S.order_fwd, S.order_bwd))
+    return e;
+  launch_update(P, 1, defer, s, false, 2);
+  launch_direction(P, 1, defer, 0, s);
+  return cuda_check("rk_pcg_entry_ssor");
+}
+
+int pcg_steps_ssor(const rk_pcg_plan& P, const rk_ssor_plan& S, int nsteps, int64_t kmax_hint, cudaStream_t s) {
+  configure_once();
+  if (int e = check_plan(P, true)) return e;
+  RK_REQUIRE(P.mode != 1 || P.ldav > 0, RK_ERR_ARG, "rk_pcg_steps_ssor: fom mode keeps A p_k columns (ldav > 0)");
+  RK_REQUIRE(kmax_hint + 2 <= P.vcap, RK_ERR_DIMENSION, "rk_pcg_steps_ssor: kmax_hint %lld beyond capacity %lld",
+             (long long)kmax_hint, (long long)P.vcap);
+  if (P.mode == 1) gemv_n_smem_ok(kmax_hint + 1);
+  const bool defer = deferred_combine(P);
+  for (int i = 0; i < nsteps; ++i) {
+    launch_spmv_pcg(P, s);
+    launch_update(P, 0, defer, s, false, 1);
+    // r_{k+1} is in P.r for odd k, in P.r2 for even k (the kernel reads st->k)
+    if (int e = launch_ssor_apply(P.A, S.dw, S.d, P.r, P.z, S.work, reinterpret_cast<int*>(S.flags), S.counters,
+                                  S.epoch + 1 + i, s, P.st, P.r2, S.order_fwd, S.order_bwd))
+      return e;
+    launch_update(P, 0, defer, s, false, 2);
+    launch_direction(P, 0, defer, kmax_hint + 1, s);
+  }
+  return cuda_check("rk_pcg_steps_ssor");
 }
 
 int pcg_curvature(const rk_pcg_plan& P, cudaStream_t s) {

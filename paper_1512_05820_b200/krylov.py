@@ -53,7 +53,7 @@ from .linalg import (
     spmv_into,
     to_numpy,
 )
-from .preconditioners import IdentityPreconditioner, JacobiPreconditioner
+from .preconditioners import IdentityPreconditioner, JacobiPreconditioner, SsorPreconditioner
 
 _BREAKDOWN_RTOL = 1e-14  # krylov.py:36 (applied on the device, spmv.cu)
 
@@ -592,16 +592,25 @@ def _augmented_pcg(op, b, yhat0, aug_basis, reduced_solver, precond, tol, *, mod
         if reduced_solver is None:
             reduced_solver = DirectReducedProjection.assemble(operator, Y)
 
-    if precond is not None and not isinstance(precond, (JacobiPreconditioner, IdentityPreconditioner)):
-        # a preconditioner without a fused form (SSOR): the reference loop,
-        # step by step, on device primitives
-        return _augmented_pcg_generic(operator, bd, Y, yh if Y is not None else None, reduced_solver, precond,
-                                      tol, mode, paper_fom_beta, relative, max_iter, sink, r0, monitor)
-
     code = _MODES.get(mode, -1)
     if code == 1 and paper_fom_beta:
         code = 2
     direct = isinstance(reduced_solver, DirectReducedProjection)
+    # SSOR runs inside the device-stepped loop (rk_pcg_*_ssor: the sweeps sit
+    # between the two halves of the update kernel) when the loop needs no host
+    # callback: its own matrix as the operator, a direct projection or none, no
+    # monitor, a known mode.
+    ssor = None
+    if isinstance(precond, SsorPreconditioner):
+        if (isinstance(operator, MatrixOperator) and operator.A is precond.A and (Y is None or direct)
+                and monitor is None and code >= 0):
+            ssor = precond
+    if precond is not None and ssor is None and not isinstance(precond, (JacobiPreconditioner, IdentityPreconditioner)):
+        # a preconditioner without a fused form here: the reference loop, step
+        # by step, on device primitives
+        return _augmented_pcg_generic(operator, bd, Y, yh if Y is not None else None, reduced_solver, precond,
+                                      tol, mode, paper_fom_beta, relative, max_iter, sink, r0, monitor)
+
     m = int(Y.shape[1]) if Y is not None else 0
     keep_av = code == 1 or keep_products
     max_iter = n if max_iter is None else int(max_iter)
@@ -622,7 +631,7 @@ def _augmented_pcg(op, b, yhat0, aug_basis, reduced_solver, precond, tol, *, mod
         run.r.copy_(bd)
     threshold = tol * norm(bd) if relative else tol
 
-    if precond is None:
+    if precond is None or ssor is not None:
         dinv = None
     elif isinstance(precond, (JacobiPreconditioner, IdentityPreconditioner)):
         dinv = precond.fused_inverse_diagonal()
@@ -637,7 +646,11 @@ def _augmented_pcg(op, b, yhat0, aug_basis, reduced_solver, precond, tol, *, mod
 
     run.write_state(threshold)
     # entry: z = M^{-1} r, ||r0||, rz, mu, p_0 (krylov.py:268,290-292)
-    nat.check(nat.lib().rk_pcg_entry(run.plan, nat.stream_ptr(device)), "augmented_pcg entry")
+    if ssor is not None:
+        nat.check(nat.lib().rk_pcg_entry_ssor(run.plan, ssor.device_plan(1), nat.stream_ptr(device)),
+                  "augmented_pcg entry (ssor)")
+    else:
+        nat.check(nat.lib().rk_pcg_entry(run.plan, nat.stream_ptr(device)), "augmented_pcg entry")
     run.read_state()
     res0 = float(run.hist[3, 0].cpu())
     if monitor is not None:
@@ -658,7 +671,7 @@ def _augmented_pcg(op, b, yhat0, aug_basis, reduced_solver, precond, tol, *, mod
     fused = isinstance(operator, MatrixOperator) and (Y is None or direct) and monitor is None
     charge_precond = precond is not None and sink is not None
     if fused:
-        k_final, status = _drive_fused(run, loop_iter, batch)
+        k_final, status = _drive_fused(run, loop_iter, batch, ssor)
     else:
         # the stepped driver charges every application as it happens, so the
         # counters a monitor snapshots (threestage Checkpoint) are the reference's
@@ -821,9 +834,10 @@ def _drive_cluster(run: _Run, max_iter: int):
         k = int(st.k)
 
 
-def _drive_fused(run: _Run, max_iter: int, batch: int | None):
-    """Batched device iterations; one 96-byte state read per batch."""
-    if nat.lib().rk_pcg_cluster_eligible(run.plan):
+def _drive_fused(run: _Run, max_iter: int, batch: int | None, ssor=None):
+    """Batched device iterations; one 96-byte state read per batch. ``ssor``:
+    the preconditioner whose sweeps run inside every step (rk_pcg_steps_ssor)."""
+    if ssor is None and nat.lib().rk_pcg_cluster_eligible(run.plan):
         return _drive_cluster(run, max_iter)
     launched = 0
     step = 4
@@ -832,8 +846,12 @@ def _drive_fused(run: _Run, max_iter: int, batch: int | None):
     while launched < max_iter:
         nb = min(step, cap, max_iter - launched)
         run.ensure(launched + nb + 1)
-        nat.check(nat.lib().rk_pcg_steps(run.plan, nb, launched + nb - 1, nat.stream_ptr(run.device)),
-                  "augmented_pcg steps")
+        if ssor is not None:
+            nat.check(nat.lib().rk_pcg_steps_ssor(run.plan, ssor.device_plan(nb), nb, launched + nb - 1,
+                                                  nat.stream_ptr(run.device)), "augmented_pcg steps (ssor)")
+        else:
+            nat.check(nat.lib().rk_pcg_steps(run.plan, nb, launched + nb - 1, nat.stream_ptr(run.device)),
+                      "augmented_pcg steps")
         launched += nb
         st = run.read_state()
         if st.done:

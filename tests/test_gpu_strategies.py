@@ -108,6 +108,53 @@ def test_ssor_on_elasticity_vs_oracle_and_deterministic(pk):
     np.testing.assert_allclose(z1, ref, rtol=1e-11, atol=1e-13 * np.abs(ref).max())
 
 
+@pytest.mark.parametrize("mode", ["cg", "fom"])
+def test_ssor_device_stepped_loop_matches_stepwise_loop(pk, mode):
+    """SSOR inside the device-stepped PCG loop (rk_pcg_steps_ssor: update of x
+    and r, forward and backward sweep, r'z and cross'z, direction, no host
+    round trip per iteration) against the reference loop taken step by step
+    with every scalar on the host (the path a monitor forces): plain and with a
+    direct projection onto a recycled basis; same iteration count, x within
+    1e-11, identical sink counters."""
+    from paper_1512_05820_b200.linalg import InstrumentationSink, scale_columns
+    from paper_1512_05820_b200.problems import elasticity_sequence
+
+    spec = next(iter(elasticity_sequence((10, 9, 8), p=1, seed=5)))
+    A = pk.SparseSpdMatrix.from_host(spec.A)
+    b = torch.from_numpy(spec.b).cuda()
+    tol = 1e-8 * float(np.linalg.norm(spec.b))
+
+    def run(stepwise, **kw):
+        sink = InstrumentationSink()
+        M = pk.build_preconditioner("ssor:1.3", A)
+        mon = (lambda k, x: None) if stepwise else None
+        res = pk.augmented_pcg(A, b, precond=M, tol=tol, mode=mode, sink=sink, monitor=mon, **kw)
+        return res, sink.snapshot()
+
+    f, cf = run(False)
+    g, cg_ = run(True)
+    assert f.converged and f.k == g.k and cf == cg_
+    assert torch.linalg.norm(f.x - g.x) <= 1e-11 * torch.linalg.norm(g.x)
+    # recycle 12 directions: stage-1 projection, then the augmented loop
+    Y = scale_columns(f.V[:, :12], np.sqrt(f.gamma[:12]))
+    b2 = b + 0.05 * torch.roll(b, 7)
+    st1 = pk.direct_reduced_solve(A, b2, Y)
+    fac = pk.BlockDiagFactor()
+    fac.append_cholesky(st1.rhat)
+    proj = pk.DirectReducedProjection(st1.aw, fac)
+
+    def run2(stepwise):
+        sink = InstrumentationSink()
+        M = pk.build_preconditioner("ssor:1.3", A)
+        mon = (lambda k, x: None) if stepwise else None
+        return pk.augmented_pcg(A, b2, st1.what, Y, proj, M, tol, mode=mode, sink=sink, monitor=mon), sink.snapshot()
+
+    f2, c2 = run2(False)
+    g2, d2 = run2(True)
+    assert f2.converged and f2.k == g2.k and c2 == d2 and f2.k < f.k
+    assert torch.linalg.norm(f2.x - g2.x) <= 1e-11 * torch.linalg.norm(g2.x)
+
+
 def test_manifest_sequence_on_device(pk):
     """f1: a reference-written manifest, loaded lazily (parse + upload of system
     j+1 on the helper thread while j solves), gives bit-identical solutions to
