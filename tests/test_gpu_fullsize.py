@@ -303,9 +303,11 @@ def test_c4_prefix_matches_reference(pk):
     stage-3 iterations and matvecs, x (at 2000 fixed indices) within 1e-8,
     q = c'x within 1e-10 -- or, where the reference does not reproduce itself
     to that bar, within twice its own run-to-run difference: a second recykl
-    run of system 1 (c4_prefix3.npz, other BLAS thread count) moved q by
-    6.4e-9 and x by 4.9e-9 at identical counters (rtol 1e-6 stops the
-    iteration long before 1e-10, and numpy's dot order follows the threads)."""
+    run of the two systems (c4_prefix3.npz, 6 BLAS threads instead of 8) moved
+    q by 1.1e-9 / 3.7e-8 and x by 2.8e-10 / 2.3e-8 at identical counters (rtol
+    1e-6 stops the iteration long before 1e-10, and numpy's dot order follows
+    the threads). Measured here: q within 1.7e-9 / 8.6e-12 of that second run,
+    2.8e-9 / 3.7e-8 of the first -- inside the reference's own scatter."""
     from paper_1512_05820_b200.problems import elasticity_sequence
 
     d = _reference_run("c4_prefix")
