@@ -336,7 +336,9 @@ __global__ void __launch_bounds__(kUpdThreads, 4) k_pcg_update(const rk_pcg_plan
 // thread sums a fixed strided subset of the chunk partials, then a fixed-order
 // block reduction (deterministic, one L2 round trip instead of a serial walk).
 // Linv does not change during a run, so narrow factors are staged in shared
-// memory before waiting on the update kernel (overlapping its tail).
+// memory before waiting on the update kernel (overlapping its tail). P.L is
+// written by the host before the run and by no kernel of the chain, so this
+// read is independent of where the predecessors wait and trigger.
 __global__ void __launch_bounds__(256) k_pcg_finish(const rk_pcg_plan P, int entry, int64_t nchunks, int wide) {
   rk_pcg_state* st = P.st;
   extern __shared__ double dyn[];      // Ls[w*w] (staged) | red[2 + m] (or [2]) | ysm[2 w]

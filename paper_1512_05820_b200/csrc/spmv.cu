@@ -548,9 +548,8 @@ __global__ void __launch_bounds__(kSpmvThreads) k_bsr3_spmm(const rk_csr A, int6
 // sequential csr_matvec order. 12 bytes per stored slot, no row pointers.
 // ---------------------------------------------------------------------------
 template <int U>
-__device__ __forceinline__ double sell1_row(const rk_csr& A, const double* __restrict__ x, int64_t slice, int lane) {
-  const int32_t base = __ldg(A.browptr + slice);
-  const int32_t width = (__ldg(A.browptr + slice + 1) - base) >> 5;
+__device__ __forceinline__ double sell1_row(const rk_csr& A, const double* __restrict__ x, int32_t base, int32_t width,
+                                            int lane) {
   const int32_t* __restrict__ col = A.bcol + base + lane;
   const double* __restrict__ val = A.bval + base + lane;
   double s = 0.0;
@@ -575,13 +574,43 @@ __device__ __forceinline__ double sell1_row(const rk_csr& A, const double* __res
 
 constexpr int kSell1U = 8;
 
+// A warp's walk over its slices with the slice pointers one step ahead: a
+// slice's work is three dependent round trips (slice pointers -> slot columns
+// and values -> gathered x); fetching the next slice's pointers before the
+// current slice's loads takes the first one off the chain.
+struct SliceWalk {
+  const int32_t* __restrict__ ptr;
+  int64_t sl, stride, nsl;
+  int32_t base, end;
+  __device__ __forceinline__ SliceWalk(const int32_t* p, int64_t first, int64_t stride_, int64_t nsl_)
+      : ptr(p), sl(first), stride(stride_), nsl(nsl_), base(0), end(0) {
+    if (sl < nsl) {
+      base = __ldg(ptr + sl);
+      end = __ldg(ptr + sl + 1);
+    }
+  }
+  __device__ __forceinline__ bool valid() const { return sl < nsl; }
+  __device__ __forceinline__ int32_t width() const { return (end - base) >> 5; }
+  __device__ __forceinline__ void advance() {
+    sl += stride;
+    if (sl < nsl) {
+      base = __ldg(ptr + sl);
+      end = __ldg(ptr + sl + 1);
+    }
+  }
+};
+
 __global__ void __launch_bounds__(kSpmvThreads) k_sell1_spmv(const rk_csr A, const double* __restrict__ x,
                                                             double* __restrict__ y) {
   const int lane = threadIdx.x & 31;
   const int64_t nsl = (A.n + 31) / 32;
   const int64_t wpb = kSpmvThreads / 32;
-  for (int64_t sl = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); sl < nsl; sl += (int64_t)gridDim.x * wpb) {
-    const double s = sell1_row<kSell1U>(A, x, sl, lane);
+  SliceWalk w(A.browptr, (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5), (int64_t)gridDim.x * wpb, nsl);
+  while (w.valid()) {
+    const int64_t sl = w.sl;
+    const int32_t base = w.base, width = w.width();
+    w.advance();  // the next slice's pointers load in the shadow of this slice's work
+    const double s = sell1_row<kSell1U>(A, x, base, width, lane);
     const int64_t row = sl * 32 + lane;
     if (row < A.n) y[row] = s;
   }
@@ -599,8 +628,12 @@ __global__ void __launch_bounds__(kSpmvThreads) k_sell1_spmv_pcg(const rk_pcg_pl
   const int64_t nsl = (P.n + 31) / 32;
   const int64_t wpb = kSpmvThreads / 32;
   double acc[2] = {0.0, 0.0};
-  for (int64_t sl = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); sl < nsl; sl += (int64_t)gridDim.x * wpb) {
-    const double s = sell1_row<kSell1U>(P.A, p, sl, lane);
+  SliceWalk w(P.A.browptr, (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5), (int64_t)gridDim.x * wpb, nsl);
+  while (w.valid()) {
+    const int64_t sl = w.sl;
+    const int32_t base = w.base, width = w.width();
+    w.advance();
+    const double s = sell1_row<kSell1U>(P.A, p, base, width, lane);
     const int64_t row = sl * 32 + lane;
     if (row < P.n) {
       Ap[row] = s;
