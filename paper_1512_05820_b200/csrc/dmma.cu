@@ -573,12 +573,17 @@ struct GramPlan {
 // bytes per flop: measured 0.91 of the DMMA peak at C5 against 0.89 for 64 x
 // 64); otherwise the 64-row tile width (48 / 64 / 80) with the least modelled
 // slot time. RK_GRAM_TILE=0..4 forces one.
-static int pick_variant(int64_t m1, int64_t m2, int64_t upper_off) {
+static int forced_variant() {
   static const int forced = [] {
     const char* e = getenv("RK_GRAM_TILE");
-    return e ? atoi(e) : -1;
+    const int v = e ? atoi(e) : -1;
+    return (v >= 0 && v < kVariants) ? v : -1;
   }();
-  if (forced >= 0 && forced < kVariants) return forced;
+  return forced;
+}
+
+static int pick_variant(int64_t m1, int64_t m2, int64_t upper_off) {
+  if (forced_variant() >= 0) return forced_variant();
   if (upper_off < 0 && m1 >= 128 && m1 % 128 == 0 && m2 % 64 == 0) return 1;
   int best = 2;
   double best_cost = 0.0;
@@ -598,8 +603,25 @@ static int pick_variant(int64_t m1, int64_t m2, int64_t upper_off) {
 // band of X and Y (L2 reuse; measured 0.80 against 0.74 of the DMMA peak on
 // the C3 truncation Gram for splits in proportion to a tile's DMMAs,
 // RK_GRAM_UNIFORM=0). Units are launched by row band, tiles within a band.
-static int build_plan(int64_t n, int64_t m1, int64_t m2, int64_t upper_off, GramPlan& P) {
-  P.which = pick_variant(m1, m2, upper_off);
+// A width that leaves at most 16 columns past the last multiple of 64 (C2's
+// truncation Gram: 386 = 6 x 64 + 2) would give the 64-wide tiling a last
+// tile column whose every tile streams full panels for one or two fragment
+// columns. Such a Gram runs as two launches: columns [0, cut) with 64-wide
+// tiles and columns [cut, m2) -- 65 to 80 of them -- as one 80-wide tile
+// column. 0: no cut (RK_GRAM_TAIL=0 disables it).
+static int64_t tail_cut(int64_t m2) {
+  static const bool on = [] {
+    const char* e = getenv("RK_GRAM_TAIL");
+    return e ? atoi(e) != 0 : true;
+  }();
+  const int64_t r = m2 % 64;
+  if (!on || forced_variant() >= 0 || m2 < 128 || r == 0 || r > 16) return 0;
+  return m2 - 64 - r;
+}
+
+// force: the variant to use, or -1 for the modelled choice.
+static int build_plan(int64_t n, int64_t m1, int64_t m2, int64_t upper_off, int force, GramPlan& P) {
+  P.which = force >= 0 ? force : pick_variant(m1, m2, upper_off);
   const GramVariant& v = gram_variant(P.which);
   const int64_t ta = (m1 + v.bm - 1) / v.bm, tb = (m2 + v.bn - 1) / v.bn;
   RK_REQUIRE(ta <= 2048 && tb <= 2048, RK_ERR_DIMENSION, "rk_gram: too many columns (%lld x %lld)",
@@ -681,7 +703,15 @@ static int build_plan(int64_t n, int64_t m1, int64_t m2, int64_t upper_off, Gram
 int64_t gram_workspace_doubles(int64_t n, int64_t m1, int64_t m2, int64_t upper_off) {
   if (m1 <= 0 || m2 <= 0) return 0;
   static thread_local GramPlan P;
-  if (build_plan(std::max<int64_t>(n, 1), m1, m2, upper_off, P) != 0) return 0;
+  n = std::max<int64_t>(n, 1);
+  const int64_t cut = tail_cut(m2);
+  if (cut > 0) {  // two launches, one after the other on the stream: they share the workspace
+    if (build_plan(n, m1, cut, upper_off, 2, P) != 0) return 0;
+    const int64_t head = P.ws_doubles;
+    if (build_plan(n, m1, m2 - cut, upper_off >= 0 ? upper_off + cut : -1, 3, P) != 0) return 0;
+    return std::max(head, P.ws_doubles);
+  }
+  if (build_plan(n, m1, m2, upper_off, -1, P) != 0) return 0;
   return P.ws_doubles;
 }
 
@@ -720,10 +750,35 @@ static int panel_map(CUtensorMap* map, const double* base, int64_t rows, int64_t
   return 0;
 }
 
+static int launch_gram_one(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m2, const double* Y,
+                           int64_t ldy, const double* Y2, int64_t ldy2, int64_t c1, double* G, int64_t ldg, double* ws,
+                           int64_t ws_len, int64_t upper_off, int force, cudaStream_t s);
+
 int launch_gram(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m2, const double* Y, int64_t ldy,
                 const double* Y2, int64_t ldy2, int64_t c1, double* G, int64_t ldg, double* ws, int64_t ws_len,
                 int64_t upper_off, cudaStream_t s) {
   if (m1 <= 0 || m2 <= 0) return 0;
+  if (Y2 == nullptr || c1 >= m2) {
+    Y2 = Y;
+    ldy2 = ldy;
+    c1 = m2;
+  }
+  const int64_t cut = tail_cut(m2);
+  if (cut <= 0) return launch_gram_one(n, m1, X, ldx, m2, Y, ldy, Y2, ldy2, c1, G, ldg, ws, ws_len, upper_off, -1, s);
+  // head: columns [0, cut), 64-wide tiles
+  if (int e = launch_gram_one(n, m1, X, ldx, cut, Y, ldy, Y2, ldy2, std::min(c1, cut), G, ldg, ws, ws_len, upper_off, 2, s))
+    return e;
+  // tail: columns [cut, m2) as one 80-wide tile column; its first buffer is
+  // whatever holds column `cut`, its boundary moves with it
+  const double* Yt = c1 > cut ? Y + cut * ldy : Y2 + (cut - c1) * ldy2;
+  const int64_t ldyt = c1 > cut ? ldy : ldy2;
+  return launch_gram_one(n, m1, X, ldx, m2 - cut, Yt, ldyt, Y2, ldy2, std::max<int64_t>(c1 - cut, 0) == 0 ? m2 - cut : c1 - cut,
+                         G + cut * ldg, ldg, ws, ws_len, upper_off >= 0 ? upper_off + cut : -1, 3, s);
+}
+
+static int launch_gram_one(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m2, const double* Y,
+                           int64_t ldy, const double* Y2, int64_t ldy2, int64_t c1, double* G, int64_t ldg, double* ws,
+                           int64_t ws_len, int64_t upper_off, int force, cudaStream_t s) {
   if (Y2 == nullptr || c1 >= m2) {
     Y2 = Y;
     ldy2 = ldy;
@@ -736,7 +791,7 @@ int launch_gram(int64_t n, int64_t m1, const double* X, int64_t ldx, int64_t m2,
   static thread_local GramPlan P;  // per calling thread (re-entrant C-ABI)
   static thread_local rk::GramUnits U;  // kernel-parameter tables, ~20 KB: never on the stack
   static thread_local rk::GramTiles T;
-  const int rc = build_plan(std::max<int64_t>(n, 1), m1, m2, upper_off, P);
+  const int rc = build_plan(std::max<int64_t>(n, 1), m1, m2, upper_off, force, P);
   if (rc != 0) return rc;
   RK_REQUIRE(P.ws_doubles == 0 || (ws && ws_len >= P.ws_doubles), RK_ERR_ARG,
              "rk_gram: workspace too small (%lld < %lld)", (long long)ws_len, (long long)P.ws_doubles);
