@@ -438,14 +438,9 @@ __global__ void __launch_bounds__(256, kDirMinBlocks)
   const int64_t mstage = m <= kStageMu ? m : 0;
   double* mus = sm;              // m (staged widths)
   double* cps = sm + mstage;     // paper-beta coefficients, k+1
-  // Before the wait: warm L2 with this thread's first row of the basis (B is
-  // fixed for the run). Safe to read now: this kernel launches once every
-  // update block has passed its own pdl_wait (wait-before-trigger, common.cuh).
-  {
-    const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (combine && i0 < P.n)
-      for (int64_t j = 0; j < m; ++j) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.B + i0 + j * P.ldb));
-  }
+  // (An L2 prefetch of each thread's first basis row before the wait changed
+  // nothing -- 269.1 vs 271.6 us per C3 iteration: the blocks of this one-wave
+  // kernel only become resident as the update kernel's blocks retire.)
   pdl_wait();
   pdl_trigger();
   if (st->done) return;
