@@ -162,12 +162,15 @@ def test_c3_sequence_within_reference_envelope(pk):
     """The bench's 40-system C3 sequence against the reference's own run of it
     (tests/golden/c3_seq.npz, oracle/run_reference_c3.py) and the reference's
     rounding envelope: recykl's own runs of the same sequence with every
-    right-hand side scaled by 1 + 1e-15 and by 1 - 1e-15
-    (c3_seq_pert*.npz, oracle/run_reference_seq.py --pert; the 40-system runs
-    take 100 minutes each, shorter earlier ones are used where they reach).
+    right-hand side scaled by 1 + 1e-15 and by 1 - 1e-15, all 40 systems each
+    (c3_seq_pert_p40.npz, c3_seq_pert_m40.npz, oracle/run_reference_seq.py
+    --pert, ~100 minutes per run; the shorter earlier runs, made with other
+    BLAS thread counts, are used too where they reach).
     The reference is chaotic at this size in CG mode: a 1e-15 perturbation
-    moves system 4 by 6 iterations, system 9 by 26 and system 18 by 44 (7.3%),
-    q = c'x by up to 6.2e-7 and x by 8.5e-7. So, per system: systems 1-3
+    moves system 4 by 6 iterations, system 9 by 26, system 18 by 44 (7.3%) and
+    systems 34-36 by 110 (26%: the drop to ~430 iterations arrives four
+    systems later or earlier), the 40-system total from 22,513 to 23,534 /
+    23,256 (ours: 23,258). So, per system: systems 1-3
     (reference swing <= 2) within +-2; every system within twice the largest
     relative swing any perturbed reference run has shown up to that system,
     plus 1%; q and x within 5x the reference's own envelope on the systems a
