@@ -245,10 +245,10 @@ def _shared_host_specs(args, seq, rank, world, dist):
         return list(seq)
     from paper_1512_05820_b200.problems import HostCsr, LinearSystemSpec
 
-    specs = list(seq)
-    if getattr(specs[0].A, "affine", None) is not None:
-        return specs  # C3: two value arrays per rank (1 GB), every system's values formed on the device
-    del specs
+    first = next(iter(seq), None)
+    if first is not None and getattr(first.A, "affine", None) is not None:
+        return list(seq)  # C3: two value arrays per rank (1 GB), every system's values formed on the device
+    del first
 
     base = os.path.join(os.environ.get("RK_BENCH_SHM", "/tmp"), f"rk_bench_{args.workload}_{args.grid}_{args.systems}")
     if rank == 0:
