@@ -4,6 +4,8 @@ residual, every run converged within the reference's tolerance, the
 truncated POD basis is A-orthonormal (Phi' A Phi = I), and the C5 POD
 basis reconstructs the snapshot energy."""
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -299,28 +301,42 @@ def test_c3_fom_matches_reference_full_size(pk):
 def test_c4_prefix_matches_reference(pk):
     """C4 (BASELINE configs[3]: 128x128x64 Q1 elasticity, K + M/dt^2, N =
     3,219,840, one invariant matrix, rtol 1e-6, pod-a-rbf cap 3000) against
-    recykl's own run of its first systems (tests/golden/c4_prefix.npz,
+    recykl's own runs of its first systems (tests/golden/c4_prefix*.npz,
     oracle/run_reference_seq.py --workload c4). System 1 is plain Jacobi PCG,
-    system 2 the stage-1 direct projection onto the 125 stored directions
-    followed by augmented CG. The north-star bar on every system: identical
-    stage-3 iterations and matvecs, x (at 2000 fixed indices) within 1e-8,
+    the later ones the stage-1 direct projection onto all stored directions
+    (125, 241, ... columns) followed by augmented CG. The north-star bar on
+    every system: identical stage-3 iterations, matvecs, preconditioner
+    applications and basis dimensions, x (at 2000 fixed indices) within 1e-8,
     q = c'x within 1e-10 -- or, where the reference does not reproduce itself
-    to that bar, within twice its own run-to-run difference: a second recykl
-    run of the two systems (c4_prefix3.npz, 6 BLAS threads instead of 8) moved
-    q by 1.1e-9 / 3.7e-8 and x by 2.8e-10 / 2.3e-8 at identical counters (rtol
+    to that bar, within twice its own run-to-run difference: recykl runs with
+    8, 6 and 5 BLAS threads differ from each other by 1.1e-9 / 3.7e-8 in q
+    and 2.8e-10 / 2.3e-8 in x on systems 1 / 2 at identical counters (rtol
     1e-6 stops the iteration long before 1e-10, and numpy's dot order follows
-    the threads). Measured here: q within 1.7e-9 / 8.6e-12 of that second run,
-    2.8e-9 / 3.7e-8 of the first -- inside the reference's own scatter."""
+    the threads). Measured on the first two systems: q within 1.7e-9 /
+    8.6e-12 of the 6-thread run, 2.8e-9 / 3.7e-8 of the 8-thread one --
+    inside the reference's own scatter."""
     from paper_1512_05820_b200.problems import elasticity_sequence
 
-    d = _reference_run("c4_prefix")
-    d2 = _reference_run("c4_prefix3")
+    runs = []
+    for name in ("c4_prefix4", "c4_prefix4b", "c4_prefix", "c4_prefix3"):
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", name + ".npz")
+        if os.path.exists(path):
+            runs.append(np.load(path))
+    if not runs:
+        pytest.skip("c4_prefix*.npz not generated (oracle/run_reference_seq.py)")
+    runs.sort(key=lambda r: -int(r["p_done"]))
+    d = runs[0]
     p = int(d["p_done"])
-    p2 = min(int(d2["p_done"]), p)
-    assert d2["iters"][:p2].tolist() == d["iters"][:p2].tolist()
-    env_q = float(np.max(np.abs(d2["q"][:p2] - d["q"][:p2]) / np.abs(d["q"][:p2])))
-    env_x = float(np.max(np.linalg.norm(d2["xs"][:p2] - d["xs"][:p2], axis=1) / np.linalg.norm(d["xs"][:p2], axis=1)))
-    tol_q, tol_x = max(1e-10, 2 * env_q), max(1e-8, 2 * env_x)
+    # the reference's own scatter per system: the largest pairwise difference of its runs,
+    # carried forward (it only grows along a recycled sequence) to systems one run covers
+    env_q, env_x = np.zeros(p), np.zeros(p)
+    for o in runs[1:]:
+        po = min(int(o["p_done"]), p)
+        assert o["iters"][:po].tolist() == d["iters"][:po].tolist()
+        env_q[:po] = np.maximum(env_q[:po], np.abs(o["q"][:po] - d["q"][:po]) / np.abs(d["q"][:po]))
+        env_x[:po] = np.maximum(env_x[:po], np.linalg.norm(o["xs"][:po] - d["xs"][:po], axis=1)
+                                / np.linalg.norm(d["xs"][:po], axis=1))
+    env_q, env_x = np.maximum.accumulate(env_q), np.maximum.accumulate(env_x)
     seq = elasticity_sequence((128, 128, 64), p=p, rtol=1e-6, seed=4, dynamic=True)
     cfg = pk.SolverConfig(truncation=pk.TruncationConfig(strategy="pod-a-rbf", nu_y=1.0, nu_w=1.0,
                                                          storage_cap=3000, max_dim=60), mode="cg")
@@ -333,6 +349,7 @@ def test_c4_prefix_matches_reference(pk):
     for j, x in enumerate(xs):
         xh = _host(x)
         q = float(seq.C[0] @ xh)
+        tol_q, tol_x = max(1e-10, 2 * env_q[j]), max(1e-8, 2 * env_x[j])
         assert abs(q - d["q"][j]) <= tol_q * abs(d["q"][j]), (j, q, d["q"][j])
         assert np.linalg.norm(xh[idx] - d["xs"][j]) <= tol_x * np.linalg.norm(d["xs"][j]), j
 

@@ -108,6 +108,30 @@ def test_ssor_on_elasticity_vs_oracle_and_deterministic(pk):
     np.testing.assert_allclose(z1, ref, rtol=1e-11, atol=1e-13 * np.abs(ref).max())
 
 
+def test_ssor_level_order_respects_dependencies(pk):
+    """rk_ssor_levels: the hand-out order of each sweep is a permutation in
+    which every row comes after the rows it depends on (strictly lower entries
+    forward, strictly upper backward) and levels are non-decreasing; the depth
+    of a 3-D 7-point stencil in natural order is nx + ny + nz - 2."""
+    from paper_1512_05820_b200.problems import laplacian3d
+
+    nx, ny, nz = 9, 7, 5
+    H = laplacian3d(nx, ny, nz)
+    A = pk.SparseSpdMatrix(H.n, H.row_offsets, H.col_indices, H.values)
+    M = pk.build_preconditioner("ssor:1.2", A)
+    assert M.depth == nx + ny + nz - 2
+    rp, ci = np.asarray(H.row_offsets), np.asarray(H.col_indices)
+    for order, upper in zip(M._order, (False, True)):
+        o = order.cpu().numpy()
+        assert sorted(o.tolist()) == list(range(H.n))
+        pos = np.empty(H.n, dtype=np.int64)
+        pos[o] = np.arange(H.n)
+        for i in range(H.n):
+            deps = ci[rp[i]:rp[i + 1]]
+            deps = deps[deps > i] if upper else deps[deps < i]
+            assert np.all(pos[deps] < pos[i])
+
+
 @pytest.mark.parametrize("mode", ["cg", "fom"])
 def test_ssor_device_stepped_loop_matches_stepwise_loop(pk, mode):
     """SSOR inside the device-stepped PCG loop (rk_pcg_steps_ssor: update of x
