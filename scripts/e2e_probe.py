@@ -28,11 +28,26 @@ _timing.phase.__enter__ = lambda self: self
 _timing.phase.__exit__ = lambda self, *a: False
 _timing.reset()
 torch.cuda.synchronize()
+ms0 = torch.cuda.memory_stats()
 t0 = time.perf_counter()
 xs, reps, _ = pk.run_sequence(hseq, cfg, precond_factory=jac)
 assert all(not hasattr(x, 'is_cuda') for x in xs)  # host inputs -> numpy solutions
 torch.cuda.synchronize()
 t = time.perf_counter() - t0
-print(json.dumps({"systems": p, "e2e_s": round(t, 3), "solve_wall_sum_s": round(sum(r.wall_time for r in reps), 3),
+ms1 = torch.cuda.memory_stats()
+alloc = {k: ms1[k] - ms0[k] for k in ("num_device_alloc", "num_device_free", "num_alloc_retries", "num_sync_all_streams")
+         if k in ms1}
+dspecs = [pk.LinearSystemSpec(A=pk.SparseSpdMatrix.from_host(s.A), b=torch.from_numpy(s.b).cuda(), xbar=None, tol=s.tol)
+          for s in specs]
+dseq = pk.SystemSequence(seq.n, dspecs, C=seq.C)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+_, dreps, _ = pk.run_sequence(dseq, cfg, precond_factory=jac)
+torch.cuda.synchronize()
+td = time.perf_counter() - t0
+print(json.dumps({"systems": p, "e2e_s": round(t, 3), "device_inputs_s": round(td, 3),
+                  "device_solve_wall_sum_s": round(sum(r.wall_time for r in dreps), 3), "allocator": alloc,
+                  "per_system_wall_ms_host_inputs": [round(1e3 * r.wall_time, 1) for r in reps[:8]],
+                  "per_system_wall_ms_device_inputs": [round(1e3 * r.wall_time, 1) for r in dreps[:8]], "solve_wall_sum_s": round(sum(r.wall_time for r in reps), 3),
                   "iters": int(sum(r.stage3_iters for r in reps)),
                   "host_timers_s": {k: round(v, 3) for k, v in _timing.TIMES.items()}}))
