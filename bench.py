@@ -42,7 +42,7 @@ warnings.simplefilter("ignore")
 
 METRIC = "sequence solve time"
 UNIT = "s"
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary_r02.json")
 
 
 def parse():

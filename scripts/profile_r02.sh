@@ -8,3 +8,5 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 python scripts/e2e_probe.py 40 > gpurun_out/r02h_e2e_probe.json 2> gpurun_out/r02h_e2e_probe.err
 cat gpurun_out/r02h_e2e_probe.json
 ls -la gpurun_out/*.ncu-rep
+# the SpMV kernel with the same build (the bench line's `traffic`)
+ncu --set full --clock-control none --import-source on -k regex:"k_bsr3_spmv_pcg" -s 70 -c 2 -o gpurun_out/prof_r02_spmv python scripts/profile_kernels.py --iters 12 > gpurun_out/prof_r02_spmv.log 2>&1
