@@ -619,8 +619,46 @@ static int64_t tail_cut(int64_t m2) {
   return m2 - 64 - r;
 }
 
-// force: the variant to use, or -1 for the modelled choice.
-static int build_plan(int64_t n, int64_t m1, int64_t m2, int64_t upper_off, int force, GramPlan& P) {
+// An upper-triangle Gram whose tiles come out 64 x 64 runs as two launches
+// when enough of it lies off the diagonal: the 128 x 64 tiles wholly above the
+// diagonal (all entries wanted: full-mode shapes), then 64 x 64 tiles for the
+// band they leave. A 128 x 64 tile moves 3/4 of the L2 -> SM bytes per flop of
+// a 64 x 64 one -- measured on full Grams, 0.95 against 0.90 of the DMMA peak
+// -- and the triangle ran at the 64 x 64 rate times its useful fraction.
+// filter 1 keeps tile (A, b) of the 128-row tiling iff A*128 + 127 <= b*64 +
+// off; filter 2 drops tile (a, b) of the 64-row tiling iff tile (a / 2, b) was
+// kept by filter 1. RK_GRAM_BAND=0 disables the split.
+struct GramPart {
+  int64_t shape_off;  // upper_off the kernel's warp shapes see (-1: every fragment)
+  int force, filter;
+  int64_t filter_off;
+};
+
+static bool above_band(int64_t A, int64_t b, int64_t off) { return A * 128 + 127 <= b * 64 + off; }
+
+static int gram_parts(int64_t m1, int64_t m2, int64_t upper_off, int force, GramPart (&parts)[2]) {
+  static const bool band = [] {
+    const char* e = getenv("RK_GRAM_BAND");
+    return e ? atoi(e) != 0 : true;
+  }();
+  const int which = force >= 0 ? force : pick_variant(m1, m2, upper_off);
+  if (band && upper_off >= 0 && which == 2 && forced_variant() < 0) {
+    int64_t above = 0;
+    for (int64_t b = 0; b * 64 < m2; ++b)
+      for (int64_t A = 0; A * 128 < m1; ++A) above += above_band(A, b, upper_off);
+    if (above >= 6) {
+      parts[0] = {-1, 1, 1, upper_off};
+      parts[1] = {upper_off, 2, 2, upper_off};
+      return 2;
+    }
+  }
+  parts[0] = {upper_off, force, 0, 0};
+  return 1;
+}
+
+// force: the variant to use, or -1 for the modelled choice. filter: see GramPart.
+static int build_plan(int64_t n, int64_t m1, int64_t m2, int64_t upper_off, int force, GramPlan& P, int filter = 0,
+                      int64_t filter_off = 0) {
   P.which = force >= 0 ? force : pick_variant(m1, m2, upper_off);
   const GramVariant& v = gram_variant(P.which);
   const int64_t ta = (m1 + v.bm - 1) / v.bm, tb = (m2 + v.bn - 1) / v.bn;
@@ -639,6 +677,8 @@ static int build_plan(int64_t n, int64_t m1, int64_t m2, int64_t upper_off, int 
   const int64_t floor_cost = (v.bm / 8) * (v.bn / 8) / 2;
   for (int64_t b = 0; b < tb; ++b)
     for (int64_t a = 0; a < ta; ++a) {
+      if (filter == 1 && !above_band(a, b, filter_off)) continue;
+      if (filter == 2 && above_band(a / 2, b, filter_off)) continue;
       const int64_t c = tile_cost(v, a, b, m1, m2, upper_off);
       if (c) {
         tiles.push_back({a, b, std::max(c, floor_cost), 1});
@@ -704,15 +744,21 @@ int64_t gram_workspace_doubles(int64_t n, int64_t m1, int64_t m2, int64_t upper_
   if (m1 <= 0 || m2 <= 0) return 0;
   static thread_local GramPlan P;
   n = std::max<int64_t>(n, 1);
+  // every launch of a Gram runs after the previous one on the stream: they share the workspace
+  auto piece = [&](int64_t mm2, int64_t off, int force) -> int64_t {
+    GramPart parts[2];
+    const int np = gram_parts(m1, mm2, off, force, parts);
+    int64_t need = 0;
+    for (int i = 0; i < np; ++i) {
+      if (build_plan(n, m1, mm2, parts[i].shape_off, parts[i].force, P, parts[i].filter, parts[i].filter_off) != 0)
+        return 0;
+      need = std::max(need, P.ws_doubles);
+    }
+    return need;
+  };
   const int64_t cut = tail_cut(m2);
-  if (cut > 0) {  // two launches, one after the other on the stream: they share the workspace
-    if (build_plan(n, m1, cut, upper_off, 2, P) != 0) return 0;
-    const int64_t head = P.ws_doubles;
-    if (build_plan(n, m1, m2 - cut, upper_off >= 0 ? upper_off + cut : -1, 3, P) != 0) return 0;
-    return std::max(head, P.ws_doubles);
-  }
-  if (build_plan(n, m1, m2, upper_off, -1, P) != 0) return 0;
-  return P.ws_doubles;
+  if (cut > 0) return std::max(piece(cut, upper_off, 2), piece(m2 - cut, upper_off >= 0 ? upper_off + cut : -1, 3));
+  return piece(m2, upper_off, -1);
 }
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
@@ -791,8 +837,14 @@ static int launch_gram_one(int64_t n, int64_t m1, const double* X, int64_t ldx, 
   static thread_local GramPlan P;  // per calling thread (re-entrant C-ABI)
   static thread_local rk::GramUnits U;  // kernel-parameter tables, ~20 KB: never on the stack
   static thread_local rk::GramTiles T;
-  const int rc = build_plan(std::max<int64_t>(n, 1), m1, m2, upper_off, force, P);
+  GramPart parts[2];
+  const int nparts = gram_parts(m1, m2, upper_off, force, parts);
+  for (int part = 0; part < nparts; ++part) {
+  const int64_t shape_off = parts[part].shape_off;
+  const int rc = build_plan(std::max<int64_t>(n, 1), m1, m2, shape_off, parts[part].force, P, parts[part].filter,
+                            parts[part].filter_off);
   if (rc != 0) return rc;
+  if (P.code.empty()) continue;
   RK_REQUIRE(P.ws_doubles == 0 || (ws && ws_len >= P.ws_doubles), RK_ERR_ARG,
              "rk_gram: workspace too small (%lld < %lld)", (long long)ws_len, (long long)P.ws_doubles);
   const GramVariant& v = gram_variant(P.which);
@@ -813,7 +865,7 @@ static int launch_gram_one(int64_t n, int64_t m1, const double* X, int64_t ldx, 
     const size_t cnt = std::min<size_t>(rk::kMaxUnits, P.code.size() - u0);
     std::copy_n(P.code.begin() + u0, cnt, U.u);
     std::copy_n(P.slot.begin() + u0, cnt, U.slot);
-    v.fn<<<(unsigned)cnt, v.threads, v.smem, s>>>(n, m1, m2, c1, G, ldg, ws, upper_off, mx, my, my2, mya, myb, U);
+    v.fn<<<(unsigned)cnt, v.threads, v.smem, s>>>(n, m1, m2, c1, G, ldg, ws, shape_off, mx, my, my2, mya, myb, U);
     rkh::note_launch();
   }
   for (size_t t0 = 0; t0 < P.split_ab.size(); t0 += rk::kMaxTiles) {
@@ -824,6 +876,7 @@ static int launch_gram_one(int64_t n, int64_t m1, const double* X, int64_t ldx, 
     v.reduce<<<dim3((unsigned)cnt, 8), 256, 0, s>>>(m1, m2, ws, G, ldg, T);
     rkh::note_launch();
   }
+  }  // parts
   return cuda_check("rk_gram");
 }
 

@@ -104,5 +104,8 @@ int main() {
     run("m16n8k8", p1688, 2.0 * 16 * 8 * 8, w, sms * 2);
     run("m16n8k16", p16816, 2.0 * 16 * 8 * 16 / 4, w, sms * 2);  // kIters/4 iterations of k16
   }
+  // One CTA per SM with 1, 2, 3, 4 warps: does a single warp reach the SM's
+  // DMMA rate, or a quarter of it (one pipe per sub-partition)?
+  for (int w : {1, 2, 3, 4, 8}) run("m8n8k4/SM", p884, 2.0 * 8 * 8 * 4, w, sms);
   return 0;
 }
